@@ -1,0 +1,216 @@
+"""float64 CPU ORACLE of the per-ray lens transport query.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import,
+call, link or execute anything under ``oracle/``.  The product package
+(``paper_2605_04017_b200``) never imports it and shares no code with it.
+
+What it computes (citations: P = /root/reference/PAPER.md, S = SPEC.md,
+O/A = SURVEY.md §8(c) steps/readings, restated in DESIGN.md):
+
+* ``trace``      -- exact sequential trace T^P (Eq. 5-7) with the
+                    validity rule of P:218, in IEEE double (oracle.c O2-O8).
+* ``map_eval``   -- factorised network {y} = f(x) if g(x) = 1 else {}
+                    with exact tanh on the blob's bf16 weights widened to double
+                    (O9-O10), symmetry canonicalisation of §4.1.
+* ``splat``      -- film accumulation of Eq. 8 / Listing 1
+                    in int64 fixed point 2^-32 (O11).
+* ``lens``       -- glass (O1), ABCD (O13), path ids (O2), ghosts (O12).
+
+Pins (tests/test_oracle_*.py) tie every function to something other than
+itself: SPEC worked values, closed forms (lensmaker, normal-incidence Fresnel),
+an independent brute-force singlet tracer, symmetry, reciprocity, ABCD
+third-order convergence, torch float64 for the MLP.  The map-vs-trace VALUE
+relation is "parity unpinned" (no trained weights exist).
+"""
+from __future__ import annotations
+
+import math
+import os
+import struct
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from . import _lib
+from .lens import (OracleLens, all_t_id, decode_path, efl_bfl, encode_path,  # noqa: F401
+                   enumerate_ghosts, ghost_id, mirrored, parse_lens, paraxial_focus_z,
+                   surface_array, abcd_vertex_to_vertex, abcd_input_to_plane, glass_index)
+
+FORWARD, BACKWARD = 0, 1
+
+
+def build():
+    return _lib.build()
+
+
+def load_lens(text: str, opts: dict | None = None) -> OracleLens:
+    """Parse + resolve lens options (sensor z NaN -> paraxial focus at lambda_ref)."""
+    o = {"input_plane_z_mm": -5.0, "sensor_z_mm": float("nan"), "sensor_w_mm": 0.0,
+         "sensor_h_mm": 0.0, "backward_exit_z_mm": -5.0, "housing_radius_mm": 0.0,
+         "lambda_ref_nm": 587.5618}
+    o.update(opts or {})
+    lens = parse_lens(text, o)
+    if math.isnan(o["sensor_z_mm"]):
+        o["sensor_z_mm"] = paraxial_focus_z(lens, o["lambda_ref_nm"])
+    lens.opts = o
+    return lens
+
+
+def _frame(lens: OracleLens, direction: int):
+    """Surface array + lens params in the traversal frame (ray travels +z at entry)."""
+    o = lens.opts
+    if direction == FORWARD:
+        S = surface_array(lens.surfaces)
+        L = np.array([o["housing_radius_mm"], o["sensor_z_mm"], o["sensor_w_mm"],
+                      o["sensor_h_mm"], 0.0, 0.0], dtype=np.float64)
+        return S, L, 0.0, +1.0
+    zS = lens.surfaces[-1].z
+    S = surface_array(mirrored(lens))
+    L = np.array([o["housing_radius_mm"], zS - o["backward_exit_z_mm"], 0.0, 0.0, 0.0, 0.0],
+                 dtype=np.float64)
+    return S, L, zS, -1.0
+
+
+def _f64(rays, k):
+    """Inputs as float64: float32 arrays are widened exactly; float64 arrays pass through."""
+    return np.ascontiguousarray(rays[k], dtype=np.float64)
+
+
+def trace(lens: OracleLens, path_id: int, direction: int, rays: dict, threads: int = 1) -> dict:
+    """Exact float64 trace of ``rays`` (float32 arrays widened) along ``path_id``.
+
+    Returns valid (bool), px, py, dx, dy, dz, I (float64) in the ORIGINAL lens
+    frame and ``margins`` (n, 4) = (geometric edge mm, |kappa|, |disc| mm^2, |w_z|).
+    """
+    S, L, zS, sgn = _frame(lens, direction)
+    ox, oy, dx, dy, dz, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm"))
+    n = ox.size
+    if sgn < 0:
+        plane_z = zS - float(rays["plane_z"])
+        dz = np.ascontiguousarray(-dz)
+    else:
+        plane_z = float(rays["plane_z"])
+    valid = np.zeros(n, np.uint8)
+    out = np.zeros((n, 6), np.float64)
+    marg = np.zeros((n, 4), np.float64)
+    lib = _lib.lib()
+    p = _lib.ptr
+
+    def run(lo, hi):
+        if hi <= lo:
+            return
+        lib.orc_trace(p(S), S.shape[0], p(L), int(path_id), hi - lo,
+                      p(ox[lo:]), p(oy[lo:]), plane_z, p(dx[lo:]), p(dy[lo:]), p(dz[lo:]),
+                      p(lam[lo:]), p(valid[lo:]), p(out[lo:]), p(marg[lo:]))
+
+    _parallel(run, n, threads)
+    res = {"valid": valid.astype(bool), "px": out[:, 0].copy(), "py": out[:, 1].copy(),
+           "dx": out[:, 2].copy(), "dy": out[:, 3].copy(), "dz": out[:, 4].copy(),
+           "I": out[:, 5].copy(), "margins": marg}
+    if sgn < 0:
+        res["dz"] = -res["dz"]
+        res["dz"][~res["valid"]] = 0.0
+    return res
+
+
+def _parallel(fn, n, threads):
+    threads = max(1, int(threads))
+    if threads == 1 or n < 4096:
+        fn(0, n)
+        return
+    step = (n + threads - 1) // threads
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda t: fn(t * step, min(n, (t + 1) * step)), range(threads)))
+
+
+# ---------------------------------------------------------------------------
+# Map blobs (format: plt_inputs/rays.py make_map_blob) -- parsed independently
+# ---------------------------------------------------------------------------
+def parse_map_blob(blob: bytes) -> dict:
+    if blob[:8] != b"PLTMAP01":
+        raise ValueError("bad map magic")
+    ver, direction, path_id, ncl, nrl = struct.unpack_from("<IIQII", blob, 8)
+    off = 8 + struct.calcsize("<IIQII")
+    norm = np.frombuffer(blob, np.float32, 20, off).astype(np.float64)
+    off += 80
+    heads = []
+    for nl in (ncl, nrl):
+        dims, Ws, Bs = [], [], []
+        for _ in range(nl):
+            fo, fi = struct.unpack_from("<II", blob, off)
+            off += 8
+            wbits = np.frombuffer(blob, np.uint16, fo * fi, off).astype(np.uint32) << 16
+            off += 2 * fo * fi
+            Ws.append(wbits.view(np.float32).astype(np.float64).reshape(fo, fi))
+            Bs.append(np.frombuffer(blob, np.float32, fo, off).astype(np.float64))
+            off += 4 * fo
+            if not dims:
+                dims.append(fi)
+            dims.append(fo)
+        heads.append({"dims": dims, "W": Ws, "b": Bs})
+    return {"version": ver, "direction": direction, "path_id": path_id, "norm": norm,
+            "classifier": heads[0], "regressor": heads[1]}
+
+
+def _head_arrays(h):
+    dims = np.array(h["dims"], dtype=np.int32)
+    W = np.ascontiguousarray(np.concatenate([w.ravel() for w in h["W"]]))
+    B = np.ascontiguousarray(np.concatenate(h["b"]))
+    return len(h["dims"]) - 1, dims, W, B
+
+
+def mlp_forward(head: dict, x: np.ndarray) -> np.ndarray:
+    """O9 on a batch x (n, dims[0]) -> (n, dims[-1])."""
+    nl, dims, W, B = _head_arrays(head)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros((x.shape[0], dims[-1]), np.float64)
+    p = _lib.ptr
+    _lib.lib().orc_mlp_forward(nl, p(dims), p(W), p(B), x.shape[0], p(x), p(y))
+    return y
+
+
+def map_eval(model, rays: dict, threads: int = 1) -> dict:
+    """O10 factorised query on float32 rays; returns valid, px..I and raw (n, 7)."""
+    m = parse_map_blob(model) if isinstance(model, (bytes, bytearray)) else model
+    ncl, cd, cW, cB = _head_arrays(m["classifier"])
+    nrl, rd, rW, rB = _head_arrays(m["regressor"])
+    norm = np.ascontiguousarray(m["norm"])
+    ox, oy, dx, dy, dz, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm"))
+    n = ox.size
+    valid = np.zeros(n, np.uint8)
+    out = np.zeros((n, 6), np.float64)
+    raw = np.zeros((n, 7), np.float64)
+    p = _lib.ptr
+    lib = _lib.lib()
+
+    def run(lo, hi):
+        if hi <= lo:
+            return
+        lib.orc_map_eval(ncl, p(cd), p(cW), p(cB), nrl, p(rd), p(rW), p(rB), p(norm), hi - lo,
+                         p(ox[lo:]), p(oy[lo:]), p(dx[lo:]), p(dy[lo:]), p(dz[lo:]), p(lam[lo:]),
+                         p(valid[lo:]), p(out[lo:]), p(raw[lo:]))
+
+    _parallel(run, n, threads)
+    return {"valid": valid.astype(bool), "px": out[:, 0].copy(), "py": out[:, 1].copy(),
+            "dx": out[:, 2].copy(), "dy": out[:, 3].copy(), "dz": out[:, 4].copy(),
+            "I": out[:, 5].copy(), "raw": raw}
+
+
+def splat(film: dict, valid, px, py, dz, I, channel=None, scale: float = 1.0):
+    """O11 int64 fixed-point film (C, H, W); returns (film, dropped)."""
+    Wd, Ht, Ch = film["width_px"], film["height_px"], film["channels"]
+    f = np.zeros((Ch, Ht, Wd), np.int64)
+    v = np.ascontiguousarray(valid, dtype=np.uint8)
+    arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (px, py, dz, I)]
+    ch = None if channel is None else np.ascontiguousarray(channel, dtype=np.uint8)
+    p = _lib.ptr
+    dropped = _lib.lib().orc_splat(Wd, Ht, Ch, film["sensor_w_mm"], film["sensor_h_mm"],
+                                   film["center_x_mm"], film["center_y_mm"], p(f), v.size, p(v),
+                                   p(arrs[0]), p(arrs[1]), p(arrs[2]), p(arrs[3]), p(ch),
+                                   np.float32(scale))
+    return f, int(dropped)
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)

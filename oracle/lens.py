@@ -1,0 +1,249 @@
+"""Oracle-side lens model, paraxial ABCD (O13), path ids (O2) and ghost enumeration (O12).
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).  Independent of the CUDA
+library's C++ parser: this file re-reads the same prescription text.
+
+Conventions: mm and nm; +z from object to image side;
+surfaces listed front to back, first vertex at z = 0, z_{k+1} = z_k + t_k;
+the glass column is the medium AFTER the surface; air (n = 1) before surface
+1; a stop has glass_after = glass_before.  Backward mode mirrors the lens
+(z' = z_S - z, R' = -R, order reversed, before/after swapped).
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GLASS_CONST, GLASS_CAUCHY, GLASS_ABBE, GLASS_SELLMEIER = 0, 1, 2, 3
+AIR = (GLASS_CONST, (1.0, 0, 0, 0, 0, 0))
+
+
+@dataclass
+class Surface:
+    z: float
+    R: float
+    a: float
+    is_stop: bool
+    glass_before: tuple = AIR
+    glass_after: tuple = AIR
+
+
+@dataclass
+class OracleLens:
+    name: str
+    surfaces: list
+    opts: dict = field(default_factory=dict)
+
+    @property
+    def optical(self):
+        return [s for s in self.surfaces if not s.is_stop]
+
+    @property
+    def n_optical(self) -> int:
+        return len(self.optical)
+
+
+def _glass_token(tok: str, vd: str | None = None):
+    t = tok.strip().lower()
+    if t == "air":
+        return AIR
+    if t == "stop":
+        return None
+    if ":" in t:
+        kind, args = t.split(":", 1)
+        v = [float(x) for x in args.split(",")]
+        if kind == "n":
+            return (GLASS_CONST, (v[0], 0, 0, 0, 0, 0))
+        if kind == "abbe":
+            return (GLASS_ABBE, (v[0], v[1], 0, 0, 0, 0))
+        if kind == "cauchy":
+            v = (v + [0.0, 0.0])[:3]
+            return (GLASS_CAUCHY, (v[0], v[1], v[2], 0, 0, 0))
+        if kind == "sellmeier":
+            return (GLASS_SELLMEIER, tuple(v[:6]))
+        raise ValueError(f"unknown glass {tok!r}")
+    nd = float(t)  # bare Kolb n_d
+    if nd == 0.0:
+        return None
+    if nd == 1.0:
+        return AIR
+    if vd is not None:
+        return (GLASS_ABBE, (nd, float(vd), 0, 0, 0, 0))
+    return (GLASS_CONST, (nd, 0, 0, 0, 0, 0))
+
+
+def parse_lens(text: str, opts: dict | None = None) -> OracleLens:
+    """Parse the repo's .lens table (or a JSON document with a 'surfaces' list)."""
+    rows, name = [], "lens"
+    if text.lstrip().startswith("{"):
+        doc = json.loads(text)
+        name = doc.get("name", name)
+        for s in doc["surfaces"]:
+            rows.append((float(s["radius_mm"]), float(s["thickness_mm"]),
+                         _glass_token(str(s["glass"])), 2.0 * float(s["semi_aperture_mm"])))
+    else:
+        for line in text.splitlines():
+            body = line.split("#", 1)[0].strip()
+            if not body:
+                continue
+            tok = body.split()
+            if tok[0] == "name":
+                name = tok[1]
+                continue
+            vd = tok[4] if len(tok) > 4 else None
+            rows.append((float(tok[0]), float(tok[1]), _glass_token(tok[2], vd), float(tok[3])))
+    surfaces, z, prev = [], 0.0, AIR
+    for (r, t, g, d) in rows:
+        stop = g is None
+        after = prev if stop else g
+        surfaces.append(Surface(z=z, R=0.0 if stop else r, a=0.5 * d, is_stop=stop,
+                                glass_before=prev, glass_after=after))
+        prev = after
+        z += t
+    lens = OracleLens(name=name, surfaces=surfaces, opts=dict(opts or {}))
+    return lens
+
+
+def glass_index(g, lam_nm: float) -> float:
+    """O1 via the C oracle (single implementation of the glass formulas)."""
+    from . import _lib
+    return _lib.glass_index(g[0], g[1], lam_nm)
+
+
+def mirrored(lens: OracleLens) -> list:
+    """C0 backward mode: z' = z_S - z, R' = -R, order reversed, before/after swapped."""
+    zS = lens.surfaces[-1].z
+    out = []
+    for s in reversed(lens.surfaces):
+        out.append(Surface(z=zS - s.z, R=-s.R if s.R != 0.0 else 0.0, a=s.a, is_stop=s.is_stop,
+                           glass_before=s.glass_after, glass_after=s.glass_before))
+    return out
+
+
+def surface_array(surfs: list) -> np.ndarray:
+    a = np.zeros((len(surfs), 18), dtype=np.float64)
+    for i, s in enumerate(surfs):
+        a[i, 0], a[i, 1], a[i, 2], a[i, 3] = s.z, s.R, s.a, 1.0 if s.is_stop else 0.0
+        a[i, 4] = s.glass_before[0]
+        a[i, 5:11] = s.glass_before[1]
+        a[i, 11] = s.glass_after[0]
+        a[i, 12:18] = s.glass_after[1]
+    return a
+
+
+# ---------------------------------------------------------------------------
+# O13 ABCD paraxial matrices
+# ray vector (h, u) with u = slope; refraction [[1,0],[(n1-n2)/(n2 R), n1/n2]];
+# translation [[1,d],[0,1]]
+# ---------------------------------------------------------------------------
+def refraction_matrix(n1: float, n2: float, R: float) -> np.ndarray:
+    c = 0.0 if R == 0.0 else (n1 - n2) / (n2 * R)
+    return np.array([[1.0, 0.0], [c, n1 / n2]])
+
+
+def translation_matrix(d: float) -> np.ndarray:
+    return np.array([[1.0, d], [0.0, 1.0]])
+
+
+def abcd_vertex_to_vertex(lens: OracleLens, lam_nm: float) -> np.ndarray:
+    """System matrix from just before the first vertex to just after the last vertex."""
+    M = np.eye(2)
+    surfs = lens.surfaces
+    for k, s in enumerate(surfs):
+        if k > 0:
+            M = translation_matrix(s.z - surfs[k - 1].z) @ M
+        n1 = glass_index(s.glass_before, lam_nm)
+        n2 = glass_index(s.glass_after, lam_nm)
+        M = refraction_matrix(n1, n2, s.R) @ M
+    return M
+
+
+def efl_bfl(lens: OracleLens, lam_nm: float):
+    """EFL = -1/C, BFL = -A/C measured from the last vertex (air on both ends)."""
+    M = abcd_vertex_to_vertex(lens, lam_nm)
+    A, C = M[0, 0], M[1, 0]
+    return -1.0 / C, -A / C
+
+
+def paraxial_focus_z(lens: OracleLens, lam_nm: float) -> float:
+    return lens.surfaces[-1].z + efl_bfl(lens, lam_nm)[1]
+
+
+def abcd_input_to_plane(lens: OracleLens, lam_nm: float, z_in: float, z_out: float) -> np.ndarray:
+    M = abcd_vertex_to_vertex(lens, lam_nm)
+    return translation_matrix(z_out - lens.surfaces[-1].z) @ M @ translation_matrix(lens.surfaces[0].z - z_in)
+
+
+# ---------------------------------------------------------------------------
+# O2 path ids (sentinel, LSB-first) and O12 ghost enumeration
+# ---------------------------------------------------------------------------
+def decode_path(path_id: int):
+    """K = floor(log2 id); interaction k (1-based) is 'R' iff bit k-1 is set."""
+    if path_id <= 0:
+        raise ValueError("path id must be positive")
+    K = path_id.bit_length() - 1
+    return ["R" if (path_id >> k) & 1 else "T" for k in range(K)]
+
+
+def encode_path(seq) -> int:
+    pid = 1 << len(seq)
+    for k, L in enumerate(seq):
+        if L == "R":
+            pid |= 1 << k
+    return pid
+
+
+def all_t_id(m: int) -> int:
+    return 1 << m
+
+
+def ghost_id(m: int, i: int, j: int) -> int:
+    """Two-bounce ghost reflecting at optical surface i then j (1 <= j < i <= m)."""
+    return (1 << (m + 2 * (i - j))) + (1 << (i - 1)) + (1 << (2 * i - j - 1))
+
+
+def _walk_normal_incidence(lens: OracleLens, path_id: int, lam_nm: float):
+    """Walk the optical-surface sequence of a path id; return throughput at normal incidence
+    (product of R = ((n1-n2)/(n1+n2))^2 or 1-R per interaction) or None if inconsistent."""
+    opt = lens.optical
+    m = len(opt)
+    seq = decode_path(path_id)
+    s, d, ncur, I = 0, +1, 1.0, 1.0
+    for L in seq:
+        if not (0 <= s < m):
+            return None
+        surf = opt[s]
+        n2 = glass_index(surf.glass_after if d > 0 else surf.glass_before, lam_nm)
+        R0 = ((ncur - n2) / (ncur + n2)) ** 2
+        if L == "T":
+            I *= 1.0 - R0
+            ncur = n2
+        else:
+            I *= R0
+            d = -d
+        s += d
+    if d < 0 or s != m:
+        return None
+    return I
+
+
+def enumerate_ghosts(lens: OracleLens, max_bounces: int = 2, min_throughput: float = 0.0,
+                     lam_nm: float = 587.5618):
+    """O12: all (i, j), 1 <= j < i <= m, ascending by id; optional normal-incidence prune.
+    max_bounces = 0 returns the all-T path only; 2 returns the all-T path plus ghosts."""
+    m = lens.n_optical
+    items = [(all_t_id(m), (0, 0))]
+    if max_bounces >= 2:
+        for i in range(2, m + 1):
+            for j in range(1, i):
+                pid = ghost_id(m, i, j)
+                if min_throughput > 0.0:
+                    thr = _walk_normal_incidence(lens, pid, lam_nm)
+                    if thr is None or thr < min_throughput:
+                        continue
+                items.append((pid, (i, j)))
+    items.sort()
+    return [p for p, _ in items], [ij for _, ij in items]
