@@ -1,0 +1,233 @@
+/*
+ * plt.h -- C ABI of libplt.so, the B200 (sm_100a) precomputed-lens-transport query library.
+ *
+ * The library answers the batched per-ray lens transport query of
+ * "Precomputed Lens Transport Maps" (arxiv 2605.04017): for each incident ray
+ * (position on an input plane, direction, wavelength) it returns an occlusion
+ * mask, the exit ray (position on the output plane, direction) and the Fresnel
+ * throughput, either by the exact sequential trace (plt_trace_rays) or by the
+ * factorised classifier/regressor network (plt_eval_map).
+ *
+ * Citations: P:n = PAPER.md line n (the paper text); S:n = SPEC.md line n;
+ * SURVEY.md §8(b)/(c) readings A1..A30 are restated in DESIGN.md.
+ *
+ * Conventions (all functions):
+ *  - Return plt_status; 0 = PLT_OK.  Never throw, never exit, never print.
+ *    On error, plt_last_error() returns a thread-local message valid until the
+ *    next plt_* call on the same thread.
+ *  - Units: millimetres and nanometres; +z runs from object side to image side;
+ *    surfaces are listed front to back with the first vertex at z = 0.
+ *  - Ray / hit / film buffers are DEVICE pointers owned by the caller (e.g.
+ *    torch.Tensor.data_ptr()); every float array must be 4-byte aligned and
+ *    hold n elements; mask_bits holds ceil(n/32) uint32 words.
+ *  - Asynchronous: compute calls enqueue on `cuda_stream` (a cudaStream_t;
+ *    NULL = legacy default stream) on the CALLER's current device and return.
+ *    Argument errors are reported synchronously; CUDA launch errors are
+ *    reported as PLT_E_CUDA; faults inside kernels surface on a later call.
+ *  - Absence is not an error: a blocked ray gets mask bit 0
+ *    and all-zero outputs.  NaN is never used as a sentinel.
+ *  - Mask bit convention: bit (i mod 32) of word i/32 is 1 <=> ray i is valid.
+ *    (This is Listing 1's `is_blocked` with the polarity reversed; A13.)
+ *  - Handles (plt_lens, plt_map) are immutable after creation and may be used
+ *    concurrently from several threads/streams/devices.
+ *  - There is no CPU fallback: every compute entry point requires an sm_100a
+ *    device and returns PLT_E_CUDA otherwise.
+ */
+#ifndef PLT_H_
+#define PLT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PLT_API __attribute__((visibility("default")))
+#else
+#define PLT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PLT_OK = 0,
+    PLT_E_INVALID_ARG = 1,  /* null / misaligned pointer, n < 0, bad enum, unknown path id     */
+    PLT_E_PARSE = 2,        /* prescription or map blob cannot be parsed (message: line/field) */
+    PLT_E_VALIDATION = 3,   /* parsed but violates an invariant (message names it)             */
+    PLT_E_CAPACITY = 4,     /* output array too small (two-call pattern, see enumerate_ghosts) */
+    PLT_E_UNSUPPORTED = 5,  /* valid request the library does not implement                    */
+    PLT_E_CUDA = 6,         /* CUDA runtime error, or no sm_100a device                        */
+    PLT_E_OOM = 7           /* host or device allocation failed                                */
+} plt_status;
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+PLT_API const char* plt_last_error(void);
+
+/* Library version string, e.g. "plt 0.1 sm_100a". */
+PLT_API const char* plt_version(void);
+
+typedef struct plt_lens plt_lens; /* opaque: parsed prescription + compiled path programs */
+typedef struct plt_map plt_map;   /* opaque: one path's factorised network (bf16 weights)  */
+
+typedef enum {
+    PLT_FORWARD = 0,  /* object side -> sensor: input plane in front, output plane = sensor */
+    PLT_BACKWARD = 1  /* sensor -> object side: rays start on the sensor (A9 separate maps) */
+} plt_dir;
+
+typedef enum {
+    PLT_FP32 = 0,  /* float32 trace + float64 re-trace of rays within a guard band of any edge */
+    PLT_FP64 = 1   /* whole trace in float64 (binding precision for ghost paths)    */
+} plt_precision;
+
+/* Lens options that are not part of the prescription. */
+typedef struct {
+    double input_plane_z_mm;   /* forward input plane z (informational; rays carry their own plane_z)     */
+    double sensor_z_mm;        /* forward output plane; NaN -> paraxial focus at lambda_ref_nm (ABCD)      */
+    double sensor_w_mm;        /* sensor rectangle ("CMOS sized rectangle"); 0 -> unbounded plane    */
+    double sensor_h_mm;
+    double backward_exit_z_mm; /* output plane for PLT_BACKWARD, in front of the first vertex (e.g. -5)    */
+    double housing_radius_mm;  /* barrel cylinder radius ("housing"); 0 -> clear apertures only     */
+    double lambda_ref_nm;      /* reference wavelength for the paraxial focus and ghost pruning (587.5618) */
+} plt_lens_opts;
+
+/*
+ * Parse and validate a lens prescription ("lens configurations are provided
+ * as JSON"; format in DESIGN.md): either the line-oriented table
+ *     name <id>
+ *     <radius_mm> <thickness_mm> <glass> <aperture_diameter_mm>
+ * (glass = air | stop | n:<n> | abbe:<nd>,<Vd> | cauchy:<A>,<B>,<C> |
+ *  sellmeier:<B1>,<B2>,<B3>,<C1>,<C2>,<C3>, or a bare Kolb n_d [V_d]) or a JSON
+ * object {"name":..,"surfaces":[{"radius_mm","thickness_mm","glass","semi_aperture_mm"}]}.
+ * text need not be NUL-terminated.  opts may be NULL (defaults above, sensor at focus).
+ * Errors: PLT_E_PARSE (line/field in message), PLT_E_VALIDATION (invariant named:
+ * more than one stop, non-positive aperture, negative thickness, |R| < aperture,
+ * index < 1 in [380,780] nm, no optical surface), PLT_E_OOM.
+ * Ownership: *out is owned by the caller and released with plt_lens_free.
+ */
+PLT_API plt_status plt_lens_load(const char* text, size_t len, const plt_lens_opts* opts, plt_lens** out);
+PLT_API void plt_lens_free(plt_lens* lens);
+
+/*
+ * Paraxial summary at lambda_nm (ABCD matrices).
+ * abcd = {A, B, C, D} from the first to the last vertex (ray vector (h, u), u = slope);
+ * efl = -1/C, bfl = -A/C (from the last vertex).  Any output pointer may be NULL.
+ * Errors: PLT_E_INVALID_ARG (lambda outside [380, 780] nm).
+ */
+PLT_API plt_status plt_lens_info(const plt_lens* lens, double lambda_nm, int* n_optical, int* stop_index,
+                         double abcd[4], double* efl_mm, double* bfl_mm, double* sensor_z_mm);
+
+/*
+ * Path ids ("Each sequence can be converted to a binary number"):
+ * id = 2^K + sum_k 2^(k-1) [interaction k is R], the stop is not an interaction.
+ * The all-transmission path of an m-surface lens is 2^m; the two-bounce ghost that
+ * reflects at optical surface i and then j (1 <= j < i <= m) is
+ * 2^(m+2(i-j)) + 2^(i-1) + 2^(2i-j-1)  (e.g. 65616 = ghost (5,3) of a 12-surface lens).
+ *
+ * plt_enumerate_ghosts lists the all-T path followed by every two-bounce ghost
+ * ("contributions from higher-order paths ... are negligible"), ascending
+ * by id.  max_bounces: 0 (all-T only) or 2.  min_throughput > 0 drops ghosts whose
+ * normal-incidence throughput R_i R_j prod T at lambda_ref is below it.
+ * ij_pairs (nullable) receives (i, j) per id ((0,0) for all-T).
+ * Two-call pattern: with ids == NULL or capacity < count, *count is set and
+ * PLT_E_CAPACITY is returned.
+ */
+PLT_API plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, double min_throughput,
+                                uint64_t* ids, int32_t* ij_pairs, int capacity, int* count);
+
+/* Device SoA input rays: origin (ox, oy, plane_z) in the lens frame, direction
+ * (dx, dy, dz) (unit; dz > 0 for PLT_FORWARD, dz < 0 for PLT_BACKWARD), wavelength
+ * in nm (caller precondition: 380..780; not checked per ray). */
+typedef struct {
+    const float* ox;
+    const float* oy;
+    const float* dx;
+    const float* dy;
+    const float* dz;
+    const float* lambda_nm;
+    double plane_z_mm;
+} plt_rays;
+
+/* Device SoA outputs (all written for every ray; zeros where invalid). */
+typedef struct {
+    uint32_t* mask_bits;  /* ceil(n/32) words, bit set <=> valid                          */
+    float* px;            /* exit position on the output plane                            */
+    float* py;
+    float* dx;            /* exit direction (unit)                                        */
+    float* dy;
+    float* dz;
+    float* throughput;    /* Fresnel throughput I_out                      */
+    uint8_t* flags;       /* nullable; trace: bit0 = re-traced in fp64 (guard band)       */
+} plt_hits;
+
+/*
+ * Exact sequential trace T^P = S_K o ... o S_1 of path `path_id` (Eq. 5-7):
+ * per surface, closest hit on the spherical/planar cap (positional operator p_sigma),
+ * clear-aperture/stop/housing test, Snell refraction or mirror reflection
+ * (directional operator d_{L,sigma}), unpolarised Fresnel R/T with Sellmeier/Abbe/
+ * Cauchy dispersion (f_{L,sigma}); valid iff sigma_{K+1} is the output plane
+ * and, for PLT_FORWARD with a sensor rectangle, the hit lies inside it.
+ * Errors: PLT_E_INVALID_ARG (null pointers, n < 0, path id inconsistent with the
+ * lens, > 48 steps), PLT_E_CUDA.  n == 0 is a no-op.
+ */
+PLT_API plt_status plt_trace_rays(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                          const plt_rays* in, const plt_hits* out, int64_t n, void* cuda_stream);
+
+/*
+ * Load one path's factorised map: a binary valid-mask classifier
+ * g: 4 -> 32 -> 32 -> 1 and a regressor f: 4 -> 32^5 -> 6, tanh hidden layers,
+ * linear outputs.  Blob layout (little-endian): magic
+ * "PLTMAP01", u32 version=1, u32 direction, u64 path_id, u32 n_cls_layers=3,
+ * u32 n_reg_layers=6, f32 in_lo[4], in_hi[4], out_mid[6], out_half[6], then per
+ * layer u32 out, u32 in, bf16 W[out][in], f32 b[out].  `lens` may be NULL (no
+ * cross-check); otherwise the blob's path id must be consistent with the lens.
+ * Errors: PLT_E_PARSE (truncated / bad magic), PLT_E_VALIDATION (dimensions), PLT_E_OOM.
+ */
+PLT_API plt_status plt_map_load(const plt_lens* lens, const void* blob, size_t len, plt_map** out);
+PLT_API void plt_map_free(plt_map* map);
+
+/*
+ * Factorised query {y} = f(x) if g(x) = 1 else {} for n rays:
+ * canonicalise by the rotation/reflection symmetry of §4.1 (Eq. 10) to
+ * x = (r, w'_x, w'_y >= 0, lambda), normalise to [-1,1], run the classifier; rays
+ * with logit >= 0 are valid and only those run the regressor (gating);
+ * outputs are de-normalised, un-reflected, rotated back, direction renormalised,
+ * throughput clamped to [0,1].  One fused sm_100a kernel: tcgen05.mma tiles with
+ * TMEM accumulators, weights resident in shared memory, inputs staged by TMA bulk copies.
+ * raw_out (nullable, device, 7*n floats, SoA: raw_out[k*n + i] with k = 0 the
+ * classifier logit and k = 1..6 the regressor outputs y before de-normalisation,
+ * y = 0 for invalid rays) exposes the network outputs for parity.
+ * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ */
+PLT_API plt_status plt_eval_map(const plt_map* map, const plt_rays* in, const plt_hits* out,
+                        float* raw_out, int64_t n, void* cuda_stream);
+
+/* Film description for sensor splatting (Eq. 8). */
+typedef struct {
+    int width_px, height_px, channels;
+    double sensor_w_mm, sensor_h_mm, center_x_mm, center_y_mm;
+} plt_film_desc;
+
+/*
+ * Splat valid hits into an int64 fixed-point film (Eq. 8; Listing 1):
+ * ix = floor((px - cx + W/2)/W * width), iy = floor((H/2 - (py - cy))/H * height)
+ * (row 0 at +y); film[c][iy][ix] += llrint(I * |dz| * weight_scale * 2^32), computed in
+ * IEEE double so the sum is exact and order independent.  Hits outside the film are
+ * dropped and counted in *dropped (device counter, nullable, incremented atomically).
+ * channel (nullable, device, n bytes) selects c (NULL -> 0); channels outside the
+ * film are dropped.  Warp-aggregated atomics (one atom.add per distinct pixel per warp).
+ * film: device, caller-owned, channels*height*width int64, NOT cleared by this call.
+ * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ */
+PLT_API plt_status plt_splat_sensor(const plt_film_desc* film_desc, int64_t* film, const plt_hits* hits,
+                            const uint8_t* channel, float weight_scale, int64_t n,
+                            unsigned long long* dropped, void* cuda_stream);
+
+/* out[i] = film[i] * 2^-32 * scale (float), for channels*height*width pixels. */
+PLT_API plt_status plt_film_resolve(const plt_film_desc* film_desc, const int64_t* film, float* out,
+                            double scale, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PLT_H_ */

@@ -1,0 +1,282 @@
+"""Python binding of libplt.so -- the B200 (sm_100a) lens-transport query library.
+
+Argument marshalling only: every step of the query runs in the library's CUDA
+kernels (``include/plt.h``).  PyTorch supplies device memory, streams and (in
+``bench.py``) process groups.  There is no CPU fallback: importing works on a
+CPU-only box, but every compute call requires the built ``libplt.so`` and an
+sm_100a device and raises otherwise.
+
+Names follow the ABI: ``Lens`` (plt_lens_load / info / enumerate_ghosts),
+``Map`` (plt_map_load), ``trace_rays``, ``eval_map``, ``splat_sensor``,
+``film_resolve``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+__all__ = ["load", "PltError", "Lens", "Map", "trace_rays", "eval_map", "splat_sensor", "film_resolve",
+           "alloc_hits", "rays_to_device", "FORWARD", "BACKWARD", "FP32", "FP64", "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libplt.so")
+FORWARD, BACKWARD = 0, 1
+FP32, FP64 = 0, 1
+
+_STATUS = {0: "PLT_OK", 1: "PLT_E_INVALID_ARG", 2: "PLT_E_PARSE", 3: "PLT_E_VALIDATION",
+           4: "PLT_E_CAPACITY", 5: "PLT_E_UNSUPPORTED", 6: "PLT_E_CUDA", 7: "PLT_E_OOM"}
+
+EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "plt_lens_info",
+            "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
+            "plt_splat_sensor", "plt_film_resolve")
+
+
+class PltError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class LensOpts(C.Structure):
+    _fields_ = [("input_plane_z_mm", C.c_double), ("sensor_z_mm", C.c_double), ("sensor_w_mm", C.c_double),
+                ("sensor_h_mm", C.c_double), ("backward_exit_z_mm", C.c_double),
+                ("housing_radius_mm", C.c_double), ("lambda_ref_nm", C.c_double)]
+
+
+class Rays(C.Structure):
+    _fields_ = [("ox", C.c_void_p), ("oy", C.c_void_p), ("dx", C.c_void_p), ("dy", C.c_void_p),
+                ("dz", C.c_void_p), ("lambda_nm", C.c_void_p), ("plane_z_mm", C.c_double)]
+
+
+class Hits(C.Structure):
+    _fields_ = [("mask_bits", C.c_void_p), ("px", C.c_void_p), ("py", C.c_void_p), ("dx", C.c_void_p),
+                ("dy", C.c_void_p), ("dz", C.c_void_p), ("throughput", C.c_void_p), ("flags", C.c_void_p)]
+
+
+class FilmDesc(C.Structure):
+    _fields_ = [("width_px", C.c_int), ("height_px", C.c_int), ("channels", C.c_int),
+                ("sensor_w_mm", C.c_double), ("sensor_h_mm", C.c_double),
+                ("center_x_mm", C.c_double), ("center_y_mm", C.c_double)]
+
+
+_lib = None
+
+
+def load():
+    """Load libplt.so (raises if it has not been built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2605_04017_b200.build` "
+                           "(the CUDA extension is required; there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    p, i, i64, u64, d, st = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_int
+    L.plt_last_error.restype = C.c_char_p
+    L.plt_version.restype = C.c_char_p
+    L.plt_lens_load.argtypes = [C.c_char_p, C.c_size_t, p, C.POINTER(p)]
+    L.plt_lens_free.argtypes = [p]
+    L.plt_lens_free.restype = None
+    L.plt_lens_info.argtypes = [p, d, p, p, p, p, p, p]
+    L.plt_enumerate_ghosts.argtypes = [p, i, d, p, p, i, p]
+    L.plt_trace_rays.argtypes = [p, u64, i, i, p, p, i64, p]
+    L.plt_map_load.argtypes = [p, C.c_char_p, C.c_size_t, C.POINTER(p)]
+    L.plt_map_free.argtypes = [p]
+    L.plt_map_free.restype = None
+    L.plt_eval_map.argtypes = [p, p, p, p, i64, p]
+    L.plt_splat_sensor.argtypes = [p, p, p, p, C.c_float, i64, p, p]
+    L.plt_film_resolve.argtypes = [p, p, p, d, p]
+    for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
+              "plt_eval_map", "plt_splat_sensor", "plt_film_resolve"):
+        getattr(L, f).restype = st
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise PltError(status, load().plt_last_error().decode(errors="replace"))
+
+
+def version() -> str:
+    return load().plt_version().decode()
+
+
+class Lens:
+    """plt_lens_load: parse + validate a prescription (.lens table or JSON)."""
+
+    def __init__(self, text: str, **opts):
+        o = LensOpts(input_plane_z_mm=opts.get("input_plane_z_mm", -5.0),
+                     sensor_z_mm=opts.get("sensor_z_mm", float("nan")),
+                     sensor_w_mm=opts.get("sensor_w_mm", 0.0), sensor_h_mm=opts.get("sensor_h_mm", 0.0),
+                     backward_exit_z_mm=opts.get("backward_exit_z_mm", -5.0),
+                     housing_radius_mm=opts.get("housing_radius_mm", 0.0),
+                     lambda_ref_nm=opts.get("lambda_ref_nm", 587.5618))
+        raw = text.encode()
+        h = C.c_void_p()
+        self._h = None
+        _check(load().plt_lens_load(raw, len(raw), C.byref(o), C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self, lambda_nm: float = 587.5618) -> dict:
+        n_opt, stop = C.c_int(), C.c_int()
+        abcd = (C.c_double * 4)()
+        efl, bfl, sz = C.c_double(), C.c_double(), C.c_double()
+        _check(load().plt_lens_info(self._h, lambda_nm, C.byref(n_opt), C.byref(stop), abcd, C.byref(efl),
+                                    C.byref(bfl), C.byref(sz)))
+        return {"n_optical": n_opt.value, "stop_index": stop.value, "abcd": list(abcd), "efl_mm": efl.value,
+                "bfl_mm": bfl.value, "sensor_z_mm": sz.value}
+
+    def enumerate_ghosts(self, max_bounces: int = 2, min_throughput: float = 0.0):
+        L = load()
+        cnt = C.c_int()
+        st = L.plt_enumerate_ghosts(self._h, max_bounces, min_throughput, None, None, 0, C.byref(cnt))
+        if st not in (0, 4):
+            _check(st)
+        ids = (C.c_uint64 * cnt.value)()
+        ij = (C.c_int32 * (2 * cnt.value))()
+        _check(L.plt_enumerate_ghosts(self._h, max_bounces, min_throughput, ids, ij, cnt.value, C.byref(cnt)))
+        return list(ids), [(ij[2 * k], ij[2 * k + 1]) for k in range(cnt.value)]
+
+    def all_t_id(self) -> int:
+        return 1 << self.info()["n_optical"]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.plt_lens_free(self._h)
+            self._h = None
+
+
+class Map:
+    """plt_map_load: one path's factorised network from a PLTMAP01 blob."""
+
+    def __init__(self, blob: bytes, lens: Lens | None = None):
+        h = C.c_void_p()
+        self._h = None
+        _check(load().plt_map_load(lens.handle if lens else None, blob, len(blob), C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.plt_map_free(self._h)
+            self._h = None
+
+
+# ---------------------------------------------------------------- marshalling helpers
+RAY_KEYS = ("ox", "oy", "dx", "dy", "dz", "lambda_nm")
+HIT_KEYS = ("px", "py", "dx", "dy", "dz", "throughput")
+
+
+def _ptr(t, n=None, dtype=None):
+    import torch
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("plt buffers must be CUDA tensors (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("plt buffers must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"expected {dtype}, got {t.dtype}")
+    if n is not None and t.numel() < n:
+        raise ValueError(f"buffer has {t.numel()} elements, need {n}")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _rays_struct(rays: dict, n: int) -> Rays:
+    import torch
+    f = torch.float32
+    return Rays(*(_ptr(rays[k], n, f) for k in RAY_KEYS), float(rays["plane_z"]))
+
+
+def _hits_struct(hits: dict, n: int) -> Hits:
+    import torch
+    f = torch.float32
+    mask = _ptr(hits["mask_bits"], (n + 31) // 32, torch.int32)
+    flags = _ptr(hits.get("flags"), n, torch.uint8) if hits.get("flags") is not None else None
+    return Hits(mask, *(_ptr(hits[k], n, f) for k in HIT_KEYS), flags)
+
+
+def alloc_hits(n: int, device="cuda", flags: bool = False) -> dict:
+    import torch
+    h = {k: torch.empty(n, dtype=torch.float32, device=device) for k in HIT_KEYS}
+    h["mask_bits"] = torch.empty((n + 31) // 32, dtype=torch.int32, device=device)
+    h["flags"] = torch.empty(n, dtype=torch.uint8, device=device) if flags else None
+    return h
+
+
+def rays_to_device(rays: dict, device="cuda", pin: bool = False) -> dict:
+    """Copy a dict of float32 numpy arrays (plt_inputs format) to device tensors."""
+    import numpy as np
+    import torch
+    out = {}
+    for k in RAY_KEYS:
+        t = torch.from_numpy(np.ascontiguousarray(rays[k], dtype=np.float32))
+        if pin:
+            t = t.pin_memory()
+        out[k] = t.to(device, non_blocking=pin)
+    out["plane_z"] = float(rays["plane_z"])
+    return out
+
+
+def _n_of(rays, n):
+    return int(rays["ox"].numel()) if n is None else int(n)
+
+
+def trace_rays(lens: Lens, path_id: int, rays: dict, hits: dict, direction: int = FORWARD,
+               precision: int = FP32, n: int | None = None, stream=None):
+    """plt_trace_rays (exact sequential trace of one path, Eq. 5-7)."""
+    n = _n_of(rays, n)
+    r, h = _rays_struct(rays, n), _hits_struct(hits, n)
+    _check(load().plt_trace_rays(lens.handle, int(path_id), direction, precision, C.byref(r), C.byref(h), n,
+                                 _stream(stream)))
+
+
+def eval_map(m: Map, rays: dict, hits: dict, raw=None, n: int | None = None, stream=None):
+    """plt_eval_map (fused classifier-gated regressor on tcgen05)."""
+    import torch
+    n = _n_of(rays, n)
+    r, h = _rays_struct(rays, n), _hits_struct(hits, n)
+    rp = _ptr(raw, 7 * n, torch.float32) if raw is not None else None
+    _check(load().plt_eval_map(m.handle, C.byref(r), C.byref(h), rp, n, _stream(stream)))
+
+
+def film_desc(d: dict) -> FilmDesc:
+    return FilmDesc(d["width_px"], d["height_px"], d["channels"], d["sensor_w_mm"], d["sensor_h_mm"],
+                    d.get("center_x_mm", 0.0), d.get("center_y_mm", 0.0))
+
+
+def splat_sensor(film_d: dict, film, hits: dict, channel=None, weight_scale: float = 1.0, n: int | None = None,
+                 dropped=None, stream=None):
+    """plt_splat_sensor (int64 fixed-point film, warp-aggregated atomics)."""
+    import torch
+    n = int(hits["px"].numel()) if n is None else int(n)
+    fd = film_desc(film_d)
+    npx = film_d["channels"] * film_d["height_px"] * film_d["width_px"]
+    h = _hits_struct(hits, n)
+    _check(load().plt_splat_sensor(C.byref(fd), _ptr(film, npx, torch.int64), C.byref(h),
+                                   _ptr(channel, n, torch.uint8) if channel is not None else None,
+                                   float(weight_scale), n,
+                                   _ptr(dropped, 1, torch.int64) if dropped is not None else None,
+                                   _stream(stream)))
+
+
+def film_resolve(film_d: dict, film, out, scale: float = 1.0, stream=None):
+    import torch
+    fd = film_desc(film_d)
+    npx = film_d["channels"] * film_d["height_px"] * film_d["width_px"]
+    _check(load().plt_film_resolve(C.byref(fd), _ptr(film, npx, torch.int64), _ptr(out, npx, torch.float32),
+                                   float(scale), _stream(stream)))

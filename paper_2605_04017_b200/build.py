@@ -1,0 +1,57 @@
+"""Build libplt.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2605_04017_b200.build [--force]
+
+Every .cu/.cpp under csrc/ is compiled with nvcc (-gencode arch=compute_100a,
+code=sm_100a, -lineinfo, -O3) and linked into paper_2605_04017_b200/libplt.so with
+the CUDA runtime linked statically (no dependency on the torch-bundled cudart).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libplt.so")
+OBJ = os.path.join(HERE, "build")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", *ARCH,
+          "-I", os.path.join(HERE, "..", "include")]
+SOURCES = ["lens.cpp", "map.cpp", "abi.cpp", "trace.cu", "splat.cu", "eval_map.cu"]
+HEADERS = ["plt_internal.h", "host.h"]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(HERE, "..", "include", "plt.h")]
+    objs = []
+    for src in SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *hdrs]):
+            extra = ["-Xptxas", "-v"] if verbose and src.endswith(".cu") else []
+            cmd = [NVCC, *COMMON, *extra, "-c", s, "-o", o]
+            if src.endswith(".cpp"):
+                cmd = [NVCC, *COMMON, "-x", "cu", "-c", s, "-o", o] if False else [NVCC, *COMMON, "-c", s, "-o", o]
+            subprocess.check_call(cmd)
+    if force or _stale(OUT, objs):
+        # version script: export only the plt_* C ABI
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs,
+                               "-Xlinker", "--exclude-libs,ALL"])
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

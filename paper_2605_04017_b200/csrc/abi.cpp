@@ -1,0 +1,199 @@
+// abi.cpp -- the extern "C" entry points of include/plt.h.
+//
+// Every entry point converts host-layer exceptions into plt_status with a
+// thread-local message, validates arguments synchronously, checks that the
+// current device is an sm_100 part and enqueues its kernels on the caller's
+// stream.  There is no CPU fallback.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "host.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+plt_status set_err(plt_status c, const std::string& m) {
+    g_err = m;
+    return c;
+}
+
+#define PLT_GUARD_BEGIN \
+    g_err.clear();      \
+    try {
+#define PLT_GUARD_END                                                   \
+    }                                                                   \
+    catch (const plt::Error& e) { return set_err(e.code, e.msg); }      \
+    catch (const std::bad_alloc&) { return set_err(PLT_E_OOM, "out of host memory"); } \
+    catch (const std::exception& e) { return set_err(PLT_E_INVALID_ARG, e.what()); }
+
+plt_status cuda_status(int e, const char* where) {
+    if (e == 0) return PLT_OK;
+    return set_err(e == (int)cudaErrorMemoryAllocation ? PLT_E_OOM : PLT_E_CUDA,
+                   std::string(where) + ": " + cudaGetErrorString((cudaError_t)e));
+}
+
+// The kernels are built for sm_100a only; refuse anything else loudly.
+plt_status check_device() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_err(PLT_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return set_err(PLT_E_CUDA, "libplt is built for sm_100a (B200); current device is sm_" +
+                                       std::to_string(major) + std::to_string(minor));
+    return PLT_OK;
+}
+
+bool rays_ok(const plt_rays* r) {
+    return r && r->ox && r->oy && r->dx && r->dy && r->dz && r->lambda_nm && std::isfinite(r->plane_z_mm);
+}
+bool hits_ok(const plt_hits* h) {
+    return h && h->mask_bits && h->px && h->py && h->dx && h->dy && h->dz && h->throughput;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* plt_last_error(void) { return g_err.c_str(); }
+
+const char* plt_version(void) { return "plt 0.1 sm_100a"; }
+
+plt_status plt_lens_load(const char* text, size_t len, const plt_lens_opts* opts, plt_lens** out) {
+    PLT_GUARD_BEGIN
+    if (!text || !out) return set_err(PLT_E_INVALID_ARG, "text and out must be non-null");
+    *out = plt::parse_lens(text, len, opts);
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
+void plt_lens_free(plt_lens* lens) { delete lens; }
+
+plt_status plt_lens_info(const plt_lens* lens, double lambda_nm, int* n_optical, int* stop_index,
+                         double abcd[4], double* efl_mm, double* bfl_mm, double* sensor_z_mm) {
+    PLT_GUARD_BEGIN
+    if (!lens) return set_err(PLT_E_INVALID_ARG, "lens is null");
+    if (!(lambda_nm >= 380.0 && lambda_nm <= 780.0))
+        return set_err(PLT_E_INVALID_ARG, "lambda_nm outside [380, 780] nm (S:60-62)");
+    double M[4];
+    plt::lens_abcd(*lens, lambda_nm, M);
+    if (n_optical) *n_optical = lens->n_optical;
+    if (stop_index) *stop_index = lens->stop_index;
+    if (abcd) std::memcpy(abcd, M, sizeof M);
+    if (efl_mm) *efl_mm = M[2] != 0.0 ? -1.0 / M[2] : INFINITY;
+    if (bfl_mm) *bfl_mm = M[2] != 0.0 ? -M[0] / M[2] : INFINITY;
+    if (sensor_z_mm) *sensor_z_mm = lens->sensor_z;
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
+plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, double min_throughput, uint64_t* ids,
+                                int32_t* ij_pairs, int capacity, int* count) {
+    PLT_GUARD_BEGIN
+    if (!lens || !count) return set_err(PLT_E_INVALID_ARG, "lens and count must be non-null");
+    if (max_bounces != 0 && max_bounces != 2)
+        return set_err(PLT_E_UNSUPPORTED, "max_bounces must be 0 or 2 (P:339: higher orders negligible)");
+    auto v = plt::enumerate_ghosts(*lens, max_bounces, min_throughput);
+    *count = (int)v.size();
+    if (!ids || capacity < (int)v.size())
+        return set_err(PLT_E_CAPACITY, "capacity " + std::to_string(capacity) + " < " + std::to_string(v.size()));
+    for (size_t i = 0; i < v.size(); ++i) {
+        ids[i] = v[i].first;
+        if (ij_pairs) { ij_pairs[2 * i] = v[i].second.first; ij_pairs[2 * i + 1] = v[i].second.second; }
+    }
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
+plt_status plt_trace_rays(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                          const plt_rays* in, const plt_hits* out, int64_t n, void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (!lens) return set_err(PLT_E_INVALID_ARG, "lens is null");
+    if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
+    if (prec != PLT_FP32 && prec != PLT_FP64) return set_err(PLT_E_INVALID_ARG, "bad precision");
+    if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
+    auto cp = plt::compile_path(*lens, path_id, (int)dir);  // validates the path id
+    if (n == 0) return PLT_OK;
+    if (!rays_ok(in) || !hits_ok(out)) return set_err(PLT_E_INVALID_ARG, "null ray/hit pointer or non-finite plane z");
+    if (n >= (int64_t)1 << 31) return set_err(PLT_E_INVALID_ARG, "n must be < 2^31 per call");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    if (prec == PLT_FP32) return cuda_status(plt::launch_trace_fp32(cp->pf, cp->pd, *in, *out, n, cuda_stream), "trace_rays");
+    return cuda_status(plt::launch_trace_fp64(cp->pd, *in, *out, n, cuda_stream), "trace_rays(fp64)");
+    PLT_GUARD_END
+}
+
+plt_status plt_map_load(const plt_lens* lens, const void* blob, size_t len, plt_map** out) {
+    PLT_GUARD_BEGIN
+    if (!blob || !out) return set_err(PLT_E_INVALID_ARG, "blob and out must be non-null");
+    *out = plt::parse_map(lens, (const uint8_t*)blob, len);
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
+void plt_map_free(plt_map* map) { delete map; }
+
+plt_status plt_eval_map(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out, int64_t n,
+                        void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (!map) return set_err(PLT_E_INVALID_ARG, "map is null");
+    if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
+    if (n == 0) return PLT_OK;
+    if (!rays_ok(in) || !hits_ok(out)) return set_err(PLT_E_INVALID_ARG, "null ray/hit pointer");
+    if (n >= (int64_t)1 << 31) return set_err(PLT_E_INVALID_ARG, "n must be < 2^31 per call");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    void* d_img = nullptr;
+    {
+        std::lock_guard<std::mutex> g(map->mu);
+        auto it = map->dev_image.find(dev);
+        if (it == map->dev_image.end()) {
+            cudaError_t e = cudaMalloc(&d_img, map->image.size());
+            if (e != cudaSuccess) return cuda_status((int)e, "eval_map weight upload");
+            e = cudaMemcpy(d_img, map->image.data(), map->image.size(), cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) { cudaFree(d_img); return cuda_status((int)e, "eval_map weight upload"); }
+            map->dev_image[dev] = d_img;
+        } else {
+            d_img = it->second;
+        }
+    }
+    return cuda_status(plt::launch_eval_map(d_img, map->layout, map->params, *in, *out, raw_out, n, cuda_stream),
+                       "eval_map");
+    PLT_GUARD_END
+}
+
+plt_status plt_splat_sensor(const plt_film_desc* fd, int64_t* film, const plt_hits* hits, const uint8_t* channel,
+                            float weight_scale, int64_t n, unsigned long long* dropped, void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (!fd || !film || !hits) return set_err(PLT_E_INVALID_ARG, "null film/hits");
+    if (fd->width_px <= 0 || fd->height_px <= 0 || fd->channels <= 0 || !(fd->sensor_w_mm > 0) || !(fd->sensor_h_mm > 0))
+        return set_err(PLT_E_INVALID_ARG, "bad film description");
+    if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
+    if (n == 0) return PLT_OK;
+    if (!hits->mask_bits || !hits->px || !hits->py || !hits->dz || !hits->throughput)
+        return set_err(PLT_E_INVALID_ARG, "null hit arrays");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    return cuda_status(plt::launch_splat(*fd, film, *hits, channel, weight_scale, n, dropped, cuda_stream), "splat_sensor");
+    PLT_GUARD_END
+}
+
+plt_status plt_film_resolve(const plt_film_desc* fd, const int64_t* film, float* out, double scale, void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (!fd || !film || !out) return set_err(PLT_E_INVALID_ARG, "null film/out");
+    if (fd->width_px <= 0 || fd->height_px <= 0 || fd->channels <= 0) return set_err(PLT_E_INVALID_ARG, "bad film description");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    return cuda_status(plt::launch_resolve(*fd, film, out, scale, cuda_stream), "film_resolve");
+    PLT_GUARD_END
+}
+
+}  // extern "C"

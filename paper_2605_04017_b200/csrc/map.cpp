@@ -1,0 +1,136 @@
+// map.cpp -- map blob parsing and packing of the factorised network for eval_map.
+//
+// Network shape: classifier 4 -> 32 -> 32 -> 1, regressor
+// 4 -> 32 -> 32 -> 32 -> 32 -> 32 -> 6, tanh hidden layers, linear outputs.
+// The bf16 weights are re-laid-out into the tcgen05 canonical K-major, no-swizzle
+// shared-memory layout: element (n, k) of a B operand with K columns lives at
+//   (n/8) * (K/8)*128 + (k/8) * 128 + (n%8) * 16 + (k%8) * 2   bytes,
+// i.e. 8-row x 16-byte core matrices, adjacent along K (LBO = 128 B) and stacked
+// along N (SBO = K/8 * 128 B).  The input layer's operand duplicates W along K so
+// one K=16 MMA consumes the bf16 hi/lo split of the 4 inputs: k 0..3 = W, 4..7 = W.
+#include <cstring>
+
+#include <cuda_runtime.h>
+
+#include "host.h"
+
+plt_map::~plt_map() {
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) return;
+    for (auto& kv : dev_image) {
+        if (!kv.second) continue;
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second);
+    }
+    cudaSetDevice(cur);
+}
+
+namespace plt {
+
+namespace {
+[[noreturn]] void fail(plt_status c, const std::string& m) { throw Error{c, m}; }
+
+struct Reader {
+    const uint8_t* p; size_t n, off = 0;
+    void need(size_t k, const char* what) {
+        if (off + k > n) fail(PLT_E_PARSE, std::string("map blob truncated while reading ") + what);
+    }
+    template <typename T> T get(const char* what) {
+        need(sizeof(T), what);
+        T v;
+        std::memcpy(&v, p + off, sizeof(T));
+        off += sizeof(T);
+        return v;
+    }
+};
+
+void pack_operand(uint8_t* dst, const uint16_t* W, int fo, int fi, int n_pad, int k_total, bool dup_input) {
+    const int sbo = (k_total / 8) * 128;
+    for (int nn = 0; nn < n_pad; ++nn)
+        for (int k = 0; k < k_total; ++k) {
+            uint16_t v = 0;
+            if (nn < fo) {
+                if (dup_input) { if (k < 2 * fi) v = W[nn * fi + (k % fi)]; }
+                else if (k < fi) v = W[nn * fi + k];
+            }
+            const size_t off = (size_t)(nn / 8) * sbo + (k / 8) * 128 + (nn % 8) * 16 + (k % 8) * 2;
+            std::memcpy(dst + off, &v, 2);
+        }
+}
+}  // namespace
+
+plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
+    Reader r{blob, len};
+    r.need(8, "magic");
+    if (std::memcmp(blob, "PLTMAP01", 8) != 0) fail(PLT_E_PARSE, "bad map magic (expected PLTMAP01)");
+    r.off = 8;
+    auto m = std::make_unique<plt_map>();
+    const uint32_t ver = r.get<uint32_t>("version");
+    if (ver != 1) fail(PLT_E_PARSE, "unsupported map version " + std::to_string(ver));
+    m->direction = r.get<uint32_t>("direction");
+    m->path_id = r.get<uint64_t>("path_id");
+    const uint32_t ncl = r.get<uint32_t>("n_cls_layers"), nrl = r.get<uint32_t>("n_reg_layers");
+    if (ncl != 3 || nrl != 6)
+        fail(PLT_E_VALIDATION, "map must have 3 classifier and 6 regressor layers (P:391-392)");
+    if (m->direction > 1) fail(PLT_E_VALIDATION, "map direction must be 0 or 1");
+    float norm[20];
+    for (int i = 0; i < 20; ++i) norm[i] = r.get<float>("normalisation");
+    for (int d = 0; d < 4; ++d) {
+        if (!(norm[4 + d] > norm[d])) fail(PLT_E_VALIDATION, "input normalisation needs hi > lo");
+        m->params.in_lo[d] = norm[d];
+        m->params.in_scale[d] = (float)(2.0 / ((double)norm[4 + d] - (double)norm[d]));
+    }
+    for (int d = 0; d < 6; ++d) { m->params.out_mid[d] = norm[8 + d]; m->params.out_half[d] = norm[14 + d]; }
+
+    static const int cls_dims[4] = {4, 32, 32, 1};
+    static const int reg_dims[7] = {4, 32, 32, 32, 32, 32, 6};
+    MapLayout& L = m->layout;
+    uint32_t off = 0;
+    auto place = [&](int n_pad, int k_total) { uint32_t o = off; off += (uint32_t)(n_pad * k_total * 2); return o; };
+    L.cls_w[0] = place(32, 16); L.cls_w[1] = place(32, 32); L.cls_w[2] = place(16, 32);
+    L.reg_w[0] = place(32, 16);
+    for (int l = 1; l < 5; ++l) L.reg_w[l] = place(32, 32);
+    L.reg_w[5] = place(16, 32);
+    L.bias_off = off;
+    uint32_t boff = 0;
+    auto bplace = [&](int cnt) { uint32_t o = boff; boff += (uint32_t)cnt; return o; };
+    L.cls_b[0] = bplace(32); L.cls_b[1] = bplace(32); L.cls_b[2] = bplace(16);
+    for (int l = 0; l < 5; ++l) L.reg_b[l] = bplace(32);
+    L.reg_b[5] = bplace(16);
+    L.total_bytes = (off + boff * 4 + 15u) & ~15u;
+    m->image.assign(L.total_bytes, 0);
+    float* bias = reinterpret_cast<float*>(m->image.data() + L.bias_off);
+
+    for (int head = 0; head < 2; ++head) {
+        const int nl = head == 0 ? 3 : 6;
+        const int* dims = head == 0 ? cls_dims : reg_dims;
+        for (int l = 0; l < nl; ++l) {
+            const uint32_t fo = r.get<uint32_t>("layer out"), fi = r.get<uint32_t>("layer in");
+            if ((int)fo != dims[l + 1] || (int)fi != dims[l])
+                fail(PLT_E_VALIDATION, std::string(head ? "regressor" : "classifier") + " layer " + std::to_string(l) +
+                                           " has dims " + std::to_string(fi) + "->" + std::to_string(fo) +
+                                           ", expected " + std::to_string(dims[l]) + "->" + std::to_string(dims[l + 1]));
+            std::vector<uint16_t> W(fo * fi);
+            r.need(2 * W.size(), "weights");
+            std::memcpy(W.data(), blob + r.off, 2 * W.size());
+            r.off += 2 * W.size();
+            const bool last = l + 1 == nl;
+            const int n_pad = last ? 16 : 32;
+            const int k_total = l == 0 ? 16 : 32;
+            const uint32_t woff = head == 0 ? L.cls_w[l] : L.reg_w[l];
+            pack_operand(m->image.data() + woff, W.data(), (int)fo, (int)fi, n_pad, k_total, l == 0);
+            const uint32_t bo = head == 0 ? L.cls_b[l] : L.reg_b[l];
+            for (uint32_t o = 0; o < fo; ++o) bias[bo + o] = r.get<float>("bias");
+        }
+    }
+    if (lens) {
+        try {
+            compile_path(*lens, m->path_id, (int)m->direction);
+        } catch (const Error& e) {
+            fail(PLT_E_VALIDATION, "map path id does not fit the lens: " + e.msg);
+        }
+    }
+    return m.release();
+}
+
+}  // namespace plt

@@ -1,0 +1,95 @@
+// plt_internal.h -- internal types shared by the host layer (lens.cpp, map.cpp, abi.cpp)
+// and the sm_100a kernels (trace.cu, eval_map.cu, splat.cu).  Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+
+#include "../../include/plt.h"
+
+namespace plt {
+
+// ---------------------------------------------------------------------------
+// Path program: the host compiles (lens, path id, direction) into a straight
+// sequence of surface steps (SURVEY.md §8(c) O2-O3 evaluated once on the host:
+// which surface the ray meets next, which interaction it takes there, which way
+// it travels).  The device executes the sequence; the program travels as a
+// __grid_constant__ kernel parameter (read through the constant bank).
+// ---------------------------------------------------------------------------
+constexpr int kMaxSteps = 40;   // two-bounce ghosts of a 12-surface lens + 3 stop crossings = 37
+
+enum StepKind : int { kSphere = 0, kPlane = 1, kStop = 2 };
+enum GlassForm : int { kCauchyForm = 0, kSellmeier = 1 };
+
+template <typename T>
+struct Step {
+    T z;        // vertex z in the traversal frame
+    T R;        // signed radius (0 for planes / stop)
+    T invR;     // 1/R (0 for planes)
+    T a2;       // clear semi-aperture squared
+    T a;        // clear semi-aperture (guard-band scaling)
+    T g[6];     // glass on the far side: Cauchy form n = g0 + g1 u + g2 u^2 (u = 1/lambda_um^2)
+                // or Sellmeier B1..B3, C1..C3 (um^2)
+    int kind;   // StepKind
+    int is_R;   // interaction: 0 = T (refract), 1 = R (reflect)
+    int dir;    // expected sign of w_z when the ray meets this surface
+    int gform;  // GlassForm
+};
+
+template <typename T>
+struct Program {
+    int n_steps;
+    int flip;         // 1 for PLT_BACKWARD: input dz and plane are mirrored, output dz negated
+    int has_rect;
+    int has_housing;
+    T z_out;          // output plane in the traversal frame
+    T z_mirror;       // zS for the backward frame (z' = zS - z)
+    T housing;        // housing radius
+    T housing2;
+    T rect_hw, rect_hh, rect_cx, rect_cy;
+    Step<T> st[kMaxSteps];
+};
+
+// ---------------------------------------------------------------------------
+// Map (factorised network) device image.  Weights are pre-packed on the host
+// into the tcgen05 "K-major, no swizzle" canonical layout (8-row x 16-byte core
+// matrices) so the kernel can TMA-copy the whole image into shared memory.
+// ---------------------------------------------------------------------------
+struct MapDims {
+    static constexpr int kHidden = 32;
+    static constexpr int kClsLayers = 3;   // 4->32, 32->32, 32->1
+    static constexpr int kRegLayers = 6;   // 4->32, 32->32 x4, 32->6
+};
+
+// Byte offsets of each packed B operand (bf16) inside the weight image.
+struct MapLayout {
+    // layer 0 (input) operands: N=32 rows, K=16 (x_hi[4], x_lo[4], 0...) -> 32*16*2 = 1024 B
+    // hidden operands:          N=32 rows, K=32                          -> 2048 B
+    // output operands:          N=16 rows, K=32                          -> 1024 B
+    uint32_t cls_w[3];
+    uint32_t reg_w[6];
+    uint32_t bias_off;     // f32 biases follow the bf16 operands
+    uint32_t cls_b[3];     // float index into bias block
+    uint32_t reg_b[6];
+    uint32_t total_bytes;  // multiple of 16
+};
+
+struct MapParams {
+    float in_lo[4], in_scale[4];   // x_hat = clamp((x - lo) * scale - 1, -1, 1), scale = 2/(hi-lo)
+    float out_mid[6], out_half[6];
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (implemented in .cu files); return cudaError_t as int.
+// ---------------------------------------------------------------------------
+int launch_trace_fp32(const Program<float>& pf, const Program<double>& pd, const plt_rays& in,
+                      const plt_hits& out, int64_t n, void* stream);
+int launch_trace_fp64(const Program<double>& pd, const plt_rays& in, const plt_hits& out,
+                      int64_t n, void* stream);
+int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
+                 float scale, int64_t n, unsigned long long* dropped, void* stream);
+int launch_resolve(const plt_film_desc& fd, const int64_t* film, float* out, double scale, void* stream);
+int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams& mp,
+                    const plt_rays& in, const plt_hits& out, float* raw, int64_t n, void* stream);
+
+}  // namespace plt

@@ -1,0 +1,102 @@
+// splat.cu -- sensor splatting into an int64 fixed-point film and film resolve (sm_100a).
+//
+// Eq. 8 accumulates I_out^P * h(x_out^P) * G over the valid
+// paths; Listing 1 adds I_out * dot(w_out, n_cmos) into the pixel of
+// p_out.  With a one-pixel box filter h and G = |w_z|, each valid hit
+// adds llrint(I * |w_z| * scale * 2^32) to film[c][iy][ix].  All arithmetic that
+// decides the pixel and the fixed-point weight is IEEE double with explicit
+// round-to-nearest intrinsics (no FMA contraction), so the integer sum is exact,
+// order independent and bit-identical across runs and GPU counts.
+//
+// Warp-aggregated atomics: lanes whose hits share a pixel find each other with
+// __match_any_sync; the lowest lane sums the group's weights from shared memory and
+// issues ONE 64-bit atom.add per distinct pixel per warp (bright compact ghosts
+// otherwise serialise on a few L2 atomic units).
+#include <cuda_runtime.h>
+
+#include "plt_internal.h"
+
+namespace plt {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void __launch_bounds__(kThreads) splat_kernel(plt_film_desc fd, int64_t* __restrict__ film,
+                                                         plt_hits hits, const uint8_t* __restrict__ channel,
+                                                         float scale, int64_t n,
+                                                         unsigned long long* dropped) {
+    __shared__ long long wsm[kThreads];
+    const int lane = threadIdx.x & 31;
+    const int warp0 = threadIdx.x & ~31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const double W = fd.sensor_w_mm, H = fd.sensor_h_mm;
+    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < n; base += stride) {
+        const int64_t i = base + lane;
+        long long key = -1, w = 0;
+        bool drop = false;
+        if (i < n) {
+            const uint32_t word = __ldg(hits.mask_bits + (i >> 5));
+            if ((word >> (i & 31)) & 1u) {
+                const double px = (double)__ldg(hits.px + i), py = (double)__ldg(hits.py + i);
+                const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn(px, fd.center_x_mm), W * 0.5), W),
+                                            (double)fd.width_px);
+                const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(H * 0.5, __dsub_rn(py, fd.center_y_mm)), H),
+                                            (double)fd.height_px);
+                const double fxf = floor(fx), fyf = floor(fy);
+                const int c = channel ? (int)__ldg(channel + i) : 0;
+                if (fxf >= 0.0 && fxf < (double)fd.width_px && fyf >= 0.0 && fyf < (double)fd.height_px &&
+                    c < fd.channels) {
+                    key = ((long long)c * fd.height_px + (long long)fyf) * fd.width_px + (long long)fxf;
+                    const double I = (double)__ldg(hits.throughput + i);
+                    const double dz = fabs((double)__ldg(hits.dz + i));
+                    w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn(I, dz), (double)scale), 4294967296.0));
+                } else {
+                    drop = true;
+                }
+            }
+        }
+        wsm[threadIdx.x] = w;
+        __syncwarp();
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(peers) - 1) {
+            long long sum = 0;
+            for (unsigned p = peers; p; p &= p - 1) sum += wsm[warp0 + __ffs(p) - 1];
+            atomicAdd(reinterpret_cast<unsigned long long*>(film + key), (unsigned long long)sum);
+        }
+        const unsigned dm = __ballot_sync(0xffffffffu, drop);
+        if (dropped && lane == 0 && dm) atomicAdd(dropped, (unsigned long long)__popc(dm));
+        __syncwarp();
+    }
+}
+
+__global__ void resolve_kernel(const int64_t* __restrict__ film, float* __restrict__ out, int64_t n, double scale) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = (float)((double)film[i] * (scale * 2.3283064365386963e-10));
+}
+
+}  // namespace
+
+int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
+                 float scale, int64_t n, unsigned long long* dropped, void* stream) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (n + kThreads - 1) / kThreads;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+    if (blocks < 1) blocks = 1;
+    splat_kernel<<<(int)blocks, kThreads, 0, (cudaStream_t)stream>>>(fd, film, hits, channel, scale, n, dropped);
+    return (int)cudaGetLastError();
+}
+
+int launch_resolve(const plt_film_desc& fd, const int64_t* film, float* out, double scale, void* stream) {
+    const int64_t n = (int64_t)fd.channels * fd.height_px * fd.width_px;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    resolve_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(film, out, n, scale);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace plt

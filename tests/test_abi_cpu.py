@@ -1,0 +1,133 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports every
+symbol include/plt.h declares, its host-only logic (parsing, validation, ABCD,
+ghost enumeration) agrees with the oracle, and compute calls fail loudly without
+an sm_100a device (no CPU fallback)."""
+import ctypes as C
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from plt_inputs import configs as CF
+from plt_inputs.lenses import LENSES
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def plt():
+    from paper_2605_04017_b200 import build
+    build.build()
+    import paper_2605_04017_b200 as p
+    p.load()
+    return p
+
+
+def test_exports_every_header_symbol(plt):
+    hdr = open(os.path.join(ROOT, "include", "plt.h")).read()
+    declared = set(re.findall(r"PLT_API[^;(]*?\b(plt_\w+)\s*\(", hdr))
+    assert len(declared) >= 12
+    lib = C.CDLL(plt.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(plt.EXPORTED)
+    assert plt.version().startswith("plt")
+
+
+@pytest.mark.parametrize("name", ["singlet", "dgauss50", "wide22", "wide24", "dgauss59"])
+def test_lens_info_matches_oracle_abcd(plt, name):
+    L = plt.Lens(LENSES[name])
+    O = oracle.load_lens(LENSES[name])
+    for lam in (486.1327, 587.5618, 656.2725, 400.0, 700.0):
+        info = L.info(lam)
+        M = oracle.abcd_vertex_to_vertex(O, lam)
+        assert np.allclose(info["abcd"], M.ravel(), rtol=1e-12, atol=1e-14)
+        efl, bfl = oracle.efl_bfl(O, lam)
+        assert abs(info["efl_mm"] - efl) < 1e-9 and abs(info["bfl_mm"] - bfl) < 1e-9
+    assert abs(L.info()["sensor_z_mm"] - O.opts["sensor_z_mm"]) < 1e-9
+    assert info["n_optical"] == O.n_optical
+
+
+@pytest.mark.parametrize("name", ["dgauss50", "wide22", "singlet"])
+def test_ghost_enumeration_matches_oracle(plt, name):
+    L = plt.Lens(LENSES[name])
+    O = oracle.load_lens(LENSES[name])
+    for mb, thr in ((0, 0.0), (2, 0.0), (2, 1e-5), (2, 1e-3)):
+        ids, ij = L.enumerate_ghosts(mb, thr)
+        oids, oij = oracle.enumerate_ghosts(O, mb, thr)
+        assert ids == oids and ij == [tuple(x) for x in oij]
+
+
+def test_two_call_capacity_pattern(plt):
+    L = plt.Lens(LENSES["wide22"])
+    lib = plt.load()
+    cnt = C.c_int()
+    st = lib.plt_enumerate_ghosts(L.handle, 2, 0.0, None, None, 0, C.byref(cnt))
+    assert st == 4 and cnt.value == 67
+    assert 65616 in L.enumerate_ghosts()[0]      # the paper's 22 mm path id
+
+
+def test_json_prescription_equals_table(plt):
+    import json
+    O = oracle.load_lens(LENSES["dgauss50"])
+    rows = []
+    for line in LENSES["dgauss50"].splitlines():
+        b = line.split("#")[0].split()
+        if not b or b[0] == "name":
+            continue
+        rows.append({"radius_mm": float(b[0]), "thickness_mm": float(b[1]), "glass": b[2],
+                     "semi_aperture_mm": float(b[3]) / 2})
+    doc = json.dumps({"name": "dg", "surfaces": rows})
+    Lj, Lt = plt.Lens(doc), plt.Lens(LENSES["dgauss50"])
+    assert Lj.info(500.0) == Lt.info(500.0)
+    assert oracle.efl_bfl(oracle.load_lens(doc), 500.0) == oracle.efl_bfl(O, 500.0)
+
+
+@pytest.mark.parametrize("text,code,frag", [
+    ("name x\n50 5 abbe:1.5 25\n", 2, "needs 2"),                       # parse error with field context
+    ("name x\n50 5 foo:1 25\n", 2, "unknown glass"),
+    ("name x\n50 5 n:1.5 oops\n", 2, "line 2"),
+    ("name x\n0 5 stop 10\n0 5 stop 10\n50 0 n:1.5 20\n", 3, "more than one aperture stop"),
+    ("name x\n5 2 n:1.5 20\n-50 0 air 20\n", 3, "semi-aperture"),         # |R| < a
+    ("name x\n50 0 n:1.5 20\n-50 0 air 20\n", 3, "non-increasing"),
+    ("name x\n50 5 n:0.9 20\n-50 0 air 20\n", 3, "index < 1"),
+    ("name x\n0 5 stop 10\n", 3, "no optical surface"),
+])
+def test_parse_and_validation_errors(plt, text, code, frag):
+    with pytest.raises(plt.PltError) as e:
+        plt.Lens(text, sensor_z_mm=50.0)
+    assert e.value.status == code and frag in str(e.value)
+
+
+def test_map_blob_validation(plt):
+    blob = CF.map_blob("C2", 1 << 10)
+    plt.Map(blob)
+    with pytest.raises(plt.PltError) as e:
+        plt.Map(blob[:100])
+    assert e.value.status == 2
+    with pytest.raises(plt.PltError) as e:
+        plt.Map(b"XXXXXXXX" + blob[8:])
+    assert e.value.status == 2
+    with pytest.raises(plt.PltError) as e:   # path 2^10 does not fit the 12-surface lens
+        plt.Map(blob, lens=plt.Lens(LENSES["wide22"]))
+    assert e.value.status == 3
+
+
+def test_compute_calls_fail_loudly_without_gpu(plt):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = plt.load()
+    L = plt.Lens(LENSES["dgauss50"])
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    rays = plt.Rays(*fake[:6], -5.0)
+    hits = plt.Hits(*fake[:7], None)
+    st = lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(rays), C.byref(hits), 10, None)
+    assert st == 6   # PLT_E_CUDA: no sm_100a device, no fallback
+    assert lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(rays), C.byref(hits), 0, None) == 0
+    assert lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(rays), C.byref(hits), -1, None) == 1
+    m = plt.Map(CF.map_blob("C2", 1 << 10))
+    assert lib.plt_eval_map(m.handle, C.byref(rays), C.byref(hits), None, 10, None) == 6
