@@ -1,0 +1,383 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched per-ray lens transport query on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl plt|reference]
+
+One STEP = one pass of the whole hot path over one batch of the
+C2 workload (BASELINE.json configs[1]: 50 mm double-Gauss, 2^24 rays per GPU,
+lambda uniform 400-700 nm, synthetic seeded rays):
+  a8  enumerate_ghosts (host; lists the lens's transport paths)
+  a6-a7 trace_rays  -- exact sequential all-T trace (fp32 + fp64 guard-band refine)
+  a1-a5 eval_map    -- fused classifier-gated regressor (tcgen05/TMEM)
+  a9  splat_sensor  -- both results splatted into an int64 film (768x512, 36x24 mm)
+  a10 film all-reduce over NCCL (N > 1)
+Every ray is queried both ways, so value = rays per step (all ranks) / step time.
+Scaling is weak: each rank owns its own chunk-aligned slice of the global index range.
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the float64 CPU oracle
+(oracle/, test infrastructure) on the host cores over a bounded sample instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "M rays/s lens-map eval & exact trace"
+UNIT = "M rays/s"
+FILM = {"width_px": 768, "height_px": 512, "channels": 1, "sensor_w_mm": 36.0, "sensor_h_mm": 24.0,
+        "center_x_mm": 0.0, "center_y_mm": 0.0}
+TANH_PER_RAY_CLS, TANH_PER_RAY_REG = 64, 160      # 2x32 classifier, 5x32 regressor hidden units
+MAC_CLS, MAC_REG = 4 * 32 + 32 * 32 + 32, 4 * 32 + 4 * 32 * 32 + 32 * 6
+IO_BYTES_PER_RAY = 6 * 4 + 6 * 4 + 1.0 / 8        # SoA in + SoA out + 1 mask bit
+MUFU_PER_CLK_PER_SM = 16                           # B200 nominal SFU rate (DESIGN.md roofline)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "plt":
+        torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if args.impl == "plt" else "gloo",
+                                device_id=torch.device("cuda", local) if args.impl == "plt" else None)
+    return ws, rank, local
+
+
+def make_workload(rank: int, n_per_rank: int):
+    from plt_inputs import configs as C
+    from plt_inputs import rays as R
+    cfg = C.CONFIGS["C2"]
+    rays = R.gen_rays(cfg["law"], cfg["seed"], rank * n_per_rank, n_per_rank)
+    return cfg, rays
+
+
+def oracle_step(olens, blob, rays, pid, threads):
+    """The oracle doing one step's work on `rays`: trace + map + splat (float64 CPU)."""
+    import oracle
+    t = oracle.trace(olens, pid, 0, rays, threads=threads)
+    m = oracle.map_eval(blob, rays, threads=threads)
+    f1, _ = oracle.splat(FILM, t["valid"], t["px"], t["py"], t["dz"], t["I"], None, 1.0)
+    f2, _ = oracle.splat(FILM, m["valid"], m["px"], m["py"], m["dz"], m["I"], None, 1.0)
+    return f1, f2
+
+
+def cpu_baseline(target_s: float = 12.0):
+    """Oracle throughput on this host's cores over a bounded sample of the C2 workload."""
+    import oracle
+    from plt_inputs import configs as C
+    from plt_inputs import rays as R
+    cfg = C.CONFIGS["C2"]
+    olens = oracle.load_lens(C.lens_text("C2"), cfg["opts"])
+    pid = 1 << olens.n_optical
+    blob = C.map_blob("C2", pid)
+    threads = oracle.host_threads()
+    n = 1 << 14
+    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
+    t0 = time.perf_counter()
+    oracle_step(olens, blob, rays, pid, threads)
+    dt = time.perf_counter() - t0
+    n2 = int(min(1 << 22, max(1 << 14, n * target_s / max(dt, 1e-3))))
+    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n2)
+    t0 = time.perf_counter()
+    oracle_step(olens, blob, rays, pid, threads)
+    dt = time.perf_counter() - t0
+    return {"value": n2 / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {n2} rays of C2 (dgauss50, all-T trace + map + splat, float64), {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------------------------------
+def run_reference(args, ws, rank):
+    """--impl reference: the float64 oracle, as it stands, on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    from plt_inputs import configs as C
+    from plt_inputs import rays as R
+    cfg = C.CONFIGS["C2"]
+    olens = oracle.load_lens(C.lens_text("C2"), cfg["opts"])
+    pid = 1 << olens.n_optical
+    blob = C.map_blob("C2", pid)
+    threads = oracle.host_threads()
+    n = args.ref_rays
+    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
+    for _ in range(args.warmup):
+        oracle_step(olens, blob, {k: (v[:4096] if k != "plane_z" else v) for k, v in rays.items()}, pid, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(olens, blob, rays, pid, threads)
+    dt = time.perf_counter() - t0
+    val = n * args.steps / dt / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C2 dgauss50 all-T trace + factorised map + splat (bounded sample)",
+                       "rays_per_step": n, "lens": "dgauss50", "path_id": pid, "lambda_nm": [400, 700]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{n} rays of C2 per step (of 2^24 per GPU in the GPU arm)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def run_plt(args, ws, rank, local):
+    import torch
+    import paper_2605_04017_b200 as plt
+    from plt_inputs import configs as C
+
+    plt.load()
+    dev = torch.device("cuda", local)
+    n = args.rays
+    cfg, rays_np = make_workload(rank, n)
+    lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
+    pid = lens.all_t_id()
+    m = plt.Map(C.map_blob("C2", pid), lens=lens)
+    stream = torch.cuda.current_stream()
+
+    # inputs resident in HBM (device-timed value); pinned host copies for e2e
+    host = {k: torch.from_numpy(rays_np[k]).pin_memory() for k in plt.RAY_KEYS}
+    d_rays = {k: host[k].to(dev) for k in plt.RAY_KEYS}
+    d_rays["plane_z"] = rays_np["plane_z"]
+    h_trace = plt.alloc_hits(n, dev)
+    h_map = plt.alloc_hits(n, dev)
+    npx = FILM["channels"] * FILM["height_px"] * FILM["width_px"]
+    film = torch.zeros(npx, dtype=torch.int64, device=dev)
+    film_host = torch.empty(npx, dtype=torch.int64).pin_memory()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    t_kern = {"trace_rays": 0.0, "eval_map": 0.0, "splat_sensor": 0.0, "film_allreduce": 0.0}
+
+    def step(ev=None):
+        lens.enumerate_ghosts(0)                       # a8 (host)
+        film.zero_()
+        if ev:
+            ev[0].record(stream)
+        plt.trace_rays(lens, pid, d_rays, h_trace, stream=stream)          # a6-a7
+        if ev:
+            ev[1].record(stream)
+        plt.eval_map(m, d_rays, h_map, stream=stream)                      # a1-a5
+        if ev:
+            ev[2].record(stream)
+        plt.splat_sensor(FILM, film, h_trace, weight_scale=1.0 / n, stream=stream)   # a9
+        plt.splat_sensor(FILM, film, h_map, weight_scale=1.0 / n, stream=stream)
+        if ev:
+            ev[3].record(stream)
+        if dist is not None:
+            dist.all_reduce(film)                                          # a10
+        if ev:
+            ev[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    elapsed = t0.elapsed_time(t1) / 1e3
+    for ev in evs:   # per-kernel durations, CUDA events on the launching stream
+        t_kern["trace_rays"] += ev[0].elapsed_time(ev[1])
+        t_kern["eval_map"] += ev[1].elapsed_time(ev[2])
+        t_kern["splat_sensor"] += ev[2].elapsed_time(ev[3])
+        t_kern["film_allreduce"] += ev[3].elapsed_time(ev[4])
+    step_s = elapsed / args.steps
+
+    # ---------------- e2e: host buffers -> device -> step -> film back to host ----------
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        for k in plt.RAY_KEYS:
+            d_rays[k].copy_(host[k], non_blocking=True)
+        step()
+        film_host.copy_(film, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = e0.elapsed_time(e1) / 1e3 / e2e_steps
+
+    # valid fractions (for the algorithmic tanh count) -- outside the timed region
+    def valid_frac(h):
+        w = h["mask_bits"].cpu().numpy().view(np.uint32)
+        return float(np.unpackbits(w.view(np.uint8)).sum()) / n
+
+    v_map, v_trace = valid_frac(h_map), valid_frac(h_trace)
+
+    vals = torch.tensor([step_s, e2e_s, elapsed], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    step_s, e2e_s, elapsed = vals.tolist()
+    if rank != 0:
+        return
+
+    peaks, peaks_src = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    per_step = {k: v / args.steps / 1e3 for k, v in t_kern.items()}
+    # eval_map roofline: MUFU (tanh) bound; algorithmic tanh = 64 per ray + 160 per valid ray
+    tanh_per_launch = n * (TANH_PER_RAY_CLS + TANH_PER_RAY_REG * v_map)
+    mufu_peak = MUFU_PER_CLK_PER_SM * 148 * sm_max * 1e6 / 1e9       # G tanh/s
+    map_ach = tanh_per_launch / per_step["eval_map"] / 1e9
+    flops_map = 2.0 * n * (MAC_CLS + MAC_REG * v_map)
+    trace_bytes = n * IO_BYTES_PER_RAY
+    kernels = {
+        "eval_map": {"ms": per_step["eval_map"] * 1e3, "M_rays_s": n / per_step["eval_map"] / 1e6,
+                     "valid_frac": v_map,
+                     "roofline": {"bound": "alu", "achieved": map_ach, "peak": mufu_peak, "unit": "Gtanh/s",
+                                  "frac": map_ach / mufu_peak,
+                                  "peak_source": "16 MUFU/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md)"},
+                     "tensor_TFLOPs": flops_map / per_step["eval_map"] / 1e12,
+                     "tensor_frac": flops_map / per_step["eval_map"] / 1e12 / float(peaks["bf16_tflops"]),
+                     "hbm_GBs": trace_bytes / per_step["eval_map"] / 1e9},
+        "trace_rays": {"ms": per_step["trace_rays"] * 1e3, "M_rays_s": n / per_step["trace_rays"] / 1e6,
+                       "valid_frac": v_trace,
+                       "roofline": {"bound": "hbm", "achieved": trace_bytes / per_step["trace_rays"] / 1e9,
+                                    "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                                    "frac": trace_bytes / per_step["trace_rays"] / 1e9 / float(peaks["hbm_gbs"]),
+                                    "note": "instruction-issue bound in practice (DESIGN.md)"}},
+        "splat_sensor": {"ms": per_step["splat_sensor"] * 1e3},
+        "film_allreduce": {"ms": per_step["film_allreduce"] * 1e3},
+    }
+    dominant = max(("eval_map", "trace_rays"), key=lambda k: kernels[k]["ms"])
+    roof = dict(kernels[dominant]["roofline"])
+    roof["kernel"] = dominant
+    roof["traffic"] = None
+    value = ws * n / step_s / 1e6
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 trace (+f64 refine), bf16xbf16->f32 map", "data": "synthetic",
+        "config": {"workload": "C2: 50 mm double-Gauss (Kolb/pbrt stand-in), 2^24 rays per GPU, "
+                               "lambda U[400,700] nm, all-T trace + factorised map (seeded Xavier bf16 "
+                               "weights) + splat" + (" + NCCL film all-reduce" if ws > 1 else ""),
+                   "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid, "film": "768x512 int64",
+                   "l2": "inputs 403 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"},
+        "roofline": roof,
+        "kernels": kernels,
+        "e2e": {"value": ws * n / e2e_s / 1e6, "unit": UNIT,
+                "h2d_bytes_per_step": 6 * 4 * n, "d2h_bytes_per_step": npx * 8},
+        "gpu_launches": args.steps * 5,
+        "clocks": clocks,
+        "peaks_source": peaks_src,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["plt", "reference"], default="plt")
+    ap.add_argument("--rays", type=int, default=1 << 24, help="rays per GPU per step")
+    ap.add_argument("--ref-rays", type=int, default=1 << 15, help="rays per oracle step (--impl reference)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, ws, rank)
+        else:
+            run_plt(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

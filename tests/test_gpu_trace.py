@@ -112,7 +112,8 @@ def test_c4_ghosts_fp64_parity(gpu_lib, cfg_name):
     for pid in pick:
         o = oracle.trace(ol, int(pid), 0, rays, threads=oracle.host_threads())
         g64 = gpu_trace(plt, gl, int(pid), rays, precision=1)
-        st = compare_trace(g64, o, tol_p=1e-6, tol_w=1e-7, tol_i=1e-9)
+        # fp64 arithmetic, float32 output storage: errors are output rounding only
+        st = compare_trace(g64, o, tol_p=4e-6, tol_w=2e-7, tol_i=2e-7)
         nval += st["n_both"]
         g32 = gpu_trace(plt, gl, int(pid), rays, precision=0)
         s32 = compare_trace(g32, o, assert_ok=False)
