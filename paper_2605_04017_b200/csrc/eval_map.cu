@@ -24,6 +24,7 @@
 //    final partial flush), so its tensor and MUFU work scales with the valid fraction.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "plt_internal.h"
 
@@ -31,29 +32,29 @@ namespace plt {
 
 namespace {
 
-constexpr int kGroups = 4;                   // tile pipelines per CTA
-constexpr int kThreads = 128 * kGroups;
 constexpr int kTile = 128;                   // rays per tile (UMMA M)
-constexpr int kQueue = 256;                  // per-group queue capacity (ring)
-constexpr int kATileBytes = 128 * 128;       // 128 rows x 64 bf16
-constexpr int kStageBytes = 6 * kTile * 4;   // six SoA slices of 128 floats
-constexpr uint32_t kMaxImageBytes = 16384;
+constexpr int kQueue = 256;                  // per-group queue capacity (ring of ray indices)
+constexpr int kAChunks = 10;                 // A row: 4 hi + 4 lo + 2 bias-ones chunks of 8 bf16
+constexpr int kARowGroupBytes = kAChunks * 128;       // SBO of the A operand
+constexpr int kATileBytes = 16 * kARowGroupBytes;     // 128 rows x 80 bf16 = 20 KB
+constexpr int kNumIn = 5;                    // staged SoA inputs: ox, oy, dx, dy, lambda (dz unused)
+constexpr int kStageBytes = kNumIn * kTile * 4;
+constexpr uint32_t kMaxImageBytes = 20480;
 
 struct GroupSmem {
-    alignas(1024) uint8_t a[kATileBytes];    // activation tile (K-major, no swizzle)
-    alignas(16) float stage[2][6][kTile];    // TMA-staged ray inputs
-    alignas(16) float qx[kQueue][4];         // queued normalised inputs
-    float qc[kQueue], qs[kQueue];            // queued rotation (cos, sin)
-    int qi[kQueue];                          // queued ray index | flip << 31
+    alignas(128) uint8_t a[kATileBytes];     // activation tile (K-major, no swizzle)
+    alignas(16) float stage[2][kNumIn][kTile];  // TMA-staged ray inputs
+    int qi[kQueue];                          // queued valid ray indices
     int wcount[4];                           // per-warp valid counts (prefix)
 };
 
+template <int G>
 struct Smem {
-    alignas(1024) uint8_t w[kMaxImageBytes];  // packed weights + biases
-    GroupSmem g[kGroups];
+    alignas(128) uint8_t w[kMaxImageBytes];   // packed weights (+ folded biases)
+    GroupSmem g[G];
     alignas(8) uint64_t bar_w;                // weights loaded
-    alignas(8) uint64_t bar_mma[kGroups];     // MMA complete
-    alignas(8) uint64_t bar_in[kGroups][2];   // input stage full
+    alignas(8) uint64_t bar_mma[G];           // MMA complete
+    alignas(8) uint64_t bar_in[G][2];         // input stage full
     uint32_t tmem_base;
 };
 
@@ -158,14 +159,16 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
 __device__ __forceinline__ float bf16lo_f(uint32_t p) { return __uint_as_float(p << 16); }
 __device__ __forceinline__ float bf16hi_f(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
 
-// A-tile addressing: element (row m, k) lives at (m/8)*1024 + (k/8)*128 + (m%8)*16 + (k%8)*2.
-__device__ __forceinline__ uint32_t a_row_off(int m) { return (uint32_t)((m >> 3) * 1024 + (m & 7) * 16); }
+// A-tile addressing: element (row m, k) lives at (m/8)*SBO + (k/8)*128 + (m%8)*16 + (k%8)*2.
+__device__ __forceinline__ uint32_t a_row_off(int m) {
+    return (uint32_t)((m >> 3) * kARowGroupBytes + (m & 7) * 16);
+}
 
-// Split 32 activations into hi/lo bf16 and store them as 8 core-matrix rows (K = 0..63).
-__device__ __forceinline__ void store_hidden(uint8_t* a, int m, const float (&h)[32]) {
-    uint8_t* row = a + a_row_off(m);
+// Split 16 activations (columns c0..c0+15) into bf16 hi/lo and store them in chunks
+// c0/8, c0/8+1 (hi, K 0..31) and 4+c0/8, 5+c0/8 (lo, K 32..63) of the row.
+__device__ __forceinline__ void store_hidden16(uint8_t* row, int c0, const float (&h)[16]) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
@@ -173,18 +176,17 @@ __device__ __forceinline__ void store_hidden(uint8_t* a, int m, const float (&h)
             hi[p] = pack_bf16(x0, x1);
             lo[p] = pack_bf16(x0 - bf16lo_f(hi[p]), x1 - bf16hi_f(hi[p]));
         }
-        *reinterpret_cast<uint4*>(row + c * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(row + (4 + c) * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<uint4*>(row + (c0 / 8 + c) * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(row + (4 + c0 / 8 + c) * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
 }
-// Input layer A row: k 0..3 = x_hi, 4..7 = x_lo, 8..15 = 0.
-__device__ __forceinline__ void store_input(uint8_t* a, int m, const float (&x)[4]) {
-    uint8_t* row = a + a_row_off(m);
+// Input-layer A row: chunk 0 = x_hi[4], x_lo[4]; chunk 1 = (1, 1, 0, ...) (folded bias hi/lo).
+__device__ __forceinline__ void store_input(uint8_t* row, const float (&x)[4]) {
     const uint32_t h01 = pack_bf16(x[0], x[1]), h23 = pack_bf16(x[2], x[3]);
     const uint32_t l01 = pack_bf16(x[0] - bf16lo_f(h01), x[1] - bf16hi_f(h01));
     const uint32_t l23 = pack_bf16(x[2] - bf16lo_f(h23), x[3] - bf16hi_f(h23));
     *reinterpret_cast<uint4*>(row) = make_uint4(h01, h23, l01, l23);
-    *reinterpret_cast<uint4*>(row + 128) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(row + 128) = make_uint4(0x3F803F80u, 0u, 0u, 0u);   // bf16 1.0, 1.0
 }
 
 struct Params {
@@ -199,36 +201,60 @@ struct Params {
     const uint8_t* wimg;   // device weight image
 };
 
-// One group's MMA for a layer: K16 steps over A (k-chunk pairs) against B.
-// a_ksteps: number of K=16 steps; b_kchunks: K/8 of the B operand (B is reused for
-// the hi and lo halves of A when a_ksteps > b_kchunks/2).
-__device__ __forceinline__ void issue_layer(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, int a_ksteps,
-                                            int b_kchunks, int n_out) {
+// Canonicalisation of §4.1 (Eq. 10): rotate p onto +x, reflect so w'_y >= 0,
+// x = (r, w'_x, w'_y, lambda) normalised to [-1, 1] (clamped).
+struct Canon { float x[4]; float c, s; bool flip; };
+__device__ __forceinline__ Canon canonicalise(const MapParams& mp, float px, float py, float wx, float wy, float lam) {
+    Canon k;
+    const float r = sqrtf(px * px + py * py);
+    if (r > 0.f) { const float ir = 1.f / r; k.c = px * ir; k.s = py * ir; }
+    else {
+        const float tt = sqrtf(wx * wx + wy * wy);
+        if (tt > 0.f) { k.c = wx / tt; k.s = wy / tt; } else { k.c = 1.f; k.s = 0.f; }
+    }
+    const float wpx = k.c * wx + k.s * wy;
+    float wpy = -k.s * wx + k.c * wy;
+    k.flip = wpy < 0.f;
+    if (k.flip) wpy = -wpy;
+    const float xin[4] = {r, wpx, wpy, lam};
+#pragma unroll
+    for (int d = 0; d < 4; ++d) k.x[d] = fminf(fmaxf((xin[d] - mp.in_lo[d]) * mp.in_scale[d] - 1.f, -1.f), 1.f);
+    return k;
+}
+
+// Layer MMAs.  Input layer: one K=16 step (x hi/lo + bias-ones).  Hidden / output
+// layers: K = 80 of A (32 hi, 32 lo, 16 bias-ones) against B = [W | W | bias chunk]
+// stored once as K = 48 (the hi and lo halves of A reuse the same W columns).
+__device__ __forceinline__ void issue_input(uint32_t tmem_d, uint32_t a_base, uint32_t b_base) {
+    umma(tmem_d, sdesc(a_base, 128, kARowGroupBytes), sdesc(b_base, 128, 256), idesc_bf16(32), 0u);
+}
+__device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, int n_out) {
     const uint32_t id = idesc_bf16(n_out);
-    const uint32_t b_sbo = (uint32_t)b_kchunks * 128;
-    const int b_steps = b_kchunks / 2;
-    for (int ks = 0; ks < a_ksteps; ++ks) {
-        const uint64_t ad = sdesc(a_base + ks * 256, 128, 1024);
-        const uint64_t bd = sdesc(b_base + (ks % b_steps) * 256, 128, b_sbo);
-        umma(tmem_d, ad, bd, id, ks > 0);
+#pragma unroll
+    for (int ks = 0; ks < 5; ++ks) {
+        const int bk = ks < 4 ? (ks & 1) : 2;
+        umma(tmem_d, sdesc(a_base + ks * 256, 128, kARowGroupBytes), sdesc(b_base + bk * 256, 128, 768), id,
+             ks > 0 ? 1u : 0u);
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) eval_map_kernel(const __grid_constant__ Params P) {
-    extern __shared__ uint8_t smem_raw[];
-    Smem& S = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+template <int G>
+__global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_constant__ Params P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Smem<G>& S = *reinterpret_cast<Smem<G>*>(smem_raw);
     const int tid = threadIdx.x;
     const int g = tid >> 7;          // group
     const int t = tid & 127;         // row within the group's tile
     const int warp = tid >> 5;
     const int q = warp & 3;          // TMEM lane quarter
     const int lane = tid & 31;
-    GroupSmem& G = S.g[g];
+    GroupSmem& Gs = S.g[g];
+    constexpr uint32_t kTmemCols = G <= 4 ? 128 : 256;
 
     // ---- setup: barriers, TMEM, weights -------------------------------------------------
     if (tid == 0) {
         mbar_init(&S.bar_w, 1);
-        for (int i = 0; i < kGroups; ++i) {
+        for (int i = 0; i < G; ++i) {
             mbar_init(&S.bar_mma[i], 1);
             mbar_init(&S.bar_in[i][0], 1);
             mbar_init(&S.bar_in[i][1], 1);
@@ -237,8 +263,15 @@ __global__ void __launch_bounds__(kThreads, 1) eval_map_kernel(const __grid_cons
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     ::"r"(smem_u32(&S.tmem_base)), "r"(32 * kGroups));
+                     ::"r"(smem_u32(&S.tmem_base)), "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // constant bias-ones chunks (8, 9) of every row of this group's A tile
+    {
+        uint8_t* row = Gs.a + a_row_off(t);
+        *reinterpret_cast<uint4*>(row + 8 * 128) = make_uint4(0x3F803F80u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(row + 9 * 128) = make_uint4(0u, 0u, 0u, 0u);
+        fence_proxy_async();
     }
     tc_fence_before();
     __syncthreads();
@@ -251,45 +284,54 @@ __global__ void __launch_bounds__(kThreads, 1) eval_map_kernel(const __grid_cons
     }
 
     const int64_t n = P.n;
-    const int64_t group_id = (int64_t)blockIdx.x * kGroups + g;
-    const int64_t group_stride = (int64_t)gridDim.x * kGroups;
+    const int64_t group_id = (int64_t)blockIdx.x * G + g;
+    const int64_t group_stride = (int64_t)gridDim.x * G;
     auto tile_full_tma = [&](int64_t tile) { return P.tma_ok && (tile + 1) * kTile <= n; };
+    auto issue_stage = [&](int64_t tile, int st) {   // one thread of the group
+        fence_proxy_async();
+        mbar_expect_tx(&S.bar_in[g][st], kStageBytes);
+        const int64_t o = tile * kTile;
+        tma_bulk_g2s(Gs.stage[st][0], P.in.ox + o, kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][1], P.in.oy + o, kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][2], P.in.dx + o, kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][3], P.in.dy + o, kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][4], P.in.lambda_nm + o, kTile * 4, &S.bar_in[g][st]);
+    };
 
-    const uint32_t a_base = smem_u32(G.a);
+    uint8_t* arow = Gs.a + a_row_off(t);
+    const uint32_t a_base = smem_u32(Gs.a);
     const uint32_t w_base = smem_u32(S.w);
-    const float* bias = reinterpret_cast<const float*>(S.w + P.lay.bias_off);
     uint32_t mma_phase = 0;
     uint32_t in_phase[2] = {0, 0};
 
-    // prologue: stage tile 0 of this group
     int64_t tile = group_id;
-    if (t == 0 && tile < P.n_tiles && tile_full_tma(tile)) {
-        mbar_expect_tx(&S.bar_in[g][0], kStageBytes);
-        const float* src[6] = {P.in.ox, P.in.oy, P.in.dx, P.in.dy, P.in.dz, P.in.lambda_nm};
-        for (int a = 0; a < 6; ++a) tma_bulk_g2s(G.stage[0][a], src[a] + tile * kTile, kTile * 4, &S.bar_in[g][0]);
-    }
+    if (t == 0 && tile < P.n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
     mbar_wait(&S.bar_w, 0);
 
-    // run one layer: A already stored + fenced by every thread; barrier; MMA; wait.
-    auto run_layer = [&](uint32_t b_off, int a_ksteps, int b_kchunks, int n_out) {
+    // A stored + fenced by every thread -> barrier -> one thread issues -> wait.
+    auto mma_layer = [&](bool input, uint32_t b_off, int n_out) {
         tc_fence_before();
         group_bar(g);
         if (t == 0) {
             tc_fence_after();
-            issue_layer(tmem, a_base, w_base + b_off, a_ksteps, b_kchunks, n_out);
+            if (input) issue_input(tmem, a_base, w_base + b_off);
+            else issue_hidden(tmem, a_base, w_base + b_off, n_out);
             umma_commit(&S.bar_mma[g]);
         }
         mbar_wait(&S.bar_mma[g], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
     };
-    // hidden epilogue: TMEM -> +bias -> tanh -> hi/lo -> A tile
-    auto hidden_epilogue = [&](const float* b) {
-        float v[32];
-        tmem_ld32(tmem_row, v);
+    // hidden epilogue: TMEM (bias already folded) -> tanh -> hi/lo -> A tile, in two halves
+    auto hidden_epilogue = [&]() {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = tanh_approx(v[j] + b[j]);
-        store_hidden(G.a, t, v);
+        for (int half = 0; half < 2; ++half) {
+            float v[16];
+            tmem_ld16(tmem_row + 16 * half, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
+            store_hidden16(arow, 16 * half, v);
+        }
         fence_proxy_async();
     };
 
@@ -297,97 +339,75 @@ __global__ void __launch_bounds__(kThreads, 1) eval_map_kernel(const __grid_cons
     // regressor over queue entries [qhead, qhead + rows), rows <= 128
     auto run_regressor = [&](int rows) {
         group_bar(g);   // publish queue entries written by other threads of the group
-        const int e = (qhead + t) & (kQueue - 1);
         const bool live = t < rows;
-        float x[4] = {0.f, 0.f, 0.f, 0.f};
-        if (live) { x[0] = G.qx[e][0]; x[1] = G.qx[e][1]; x[2] = G.qx[e][2]; x[3] = G.qx[e][3]; }
-        const float c = live ? G.qc[e] : 1.f, s = live ? G.qs[e] : 0.f;
-        const int qi = live ? G.qi[e] : 0;
-        store_input(G.a, t, x);
-        fence_proxy_async();
-        run_layer(P.lay.reg_w[0], 1, 2, 32);
-        hidden_epilogue(bias + P.lay.reg_b[0]);
-        for (int l = 1; l < 5; ++l) {
-            run_layer(P.lay.reg_w[l], 4, 4, 32);
-            hidden_epilogue(bias + P.lay.reg_b[l]);
+        const int qi = live ? Gs.qi[(qhead + t) & (kQueue - 1)] : 0;
+        float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
+        if (live) {
+            px = __ldg(P.in.ox + qi); py = __ldg(P.in.oy + qi); wx = __ldg(P.in.dx + qi);
+            wy = __ldg(P.in.dy + qi); lam = __ldg(P.in.lambda_nm + qi);
         }
-        run_layer(P.lay.reg_w[5], 4, 4, 16);
+        const Canon k = canonicalise(P.mp, px, py, wx, wy, lam);
+        store_input(arow, k.x);
+        fence_proxy_async();
+        mma_layer(true, P.lay.reg_w[0], 32);
+        hidden_epilogue();
+#pragma unroll 1
+        for (int l = 1; l < 5; ++l) {
+            mma_layer(false, P.lay.reg_w[l], 32);
+            hidden_epilogue();
+        }
+        mma_layer(false, P.lay.reg_w[5], 16);
         float y[16];
         tmem_ld16(tmem_row, y);
         if (live) {
-            const float* b5 = bias + P.lay.reg_b[5];
             float o[6];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) { y[d] += b5[d]; o[d] = P.mp.out_mid[d] + P.mp.out_half[d] * y[d]; }
-            const int64_t i = (int64_t)(qi & 0x7FFFFFFF);
-            if (qi < 0) { o[1] = -o[1]; o[3] = -o[3]; }  // undo the reflection
-            const float px = c * o[0] - s * o[1], py = s * o[0] + c * o[1];
-            float wx = c * o[2] - s * o[3], wy = s * o[2] + c * o[3], wz = o[4];
-            const float inv = rsqrtf(wx * wx + wy * wy + wz * wz);
-            P.out.px[i] = px; P.out.py[i] = py;
-            P.out.dx[i] = wx * inv; P.out.dy[i] = wy * inv; P.out.dz[i] = wz * inv;
-            P.out.throughput[i] = fminf(fmaxf(o[5], 0.f), 1.f);
+            for (int d = 0; d < 6; ++d) o[d] = P.mp.out_mid[d] + P.mp.out_half[d] * y[d];
+            if (k.flip) { o[1] = -o[1]; o[3] = -o[3]; }  // undo the reflection
+            const float ox = k.c * o[0] - k.s * o[1], oy = k.s * o[0] + k.c * o[1];
+            const float wx2 = k.c * o[2] - k.s * o[3], wy2 = k.s * o[2] + k.c * o[3], wz2 = o[4];
+            const float inv = rsqrtf(wx2 * wx2 + wy2 * wy2 + wz2 * wz2);
+            P.out.px[qi] = ox; P.out.py[qi] = oy;
+            P.out.dx[qi] = wx2 * inv; P.out.dy[qi] = wy2 * inv; P.out.dz[qi] = wz2 * inv;
+            P.out.throughput[qi] = fminf(fmaxf(o[5], 0.f), 1.f);
             if (P.raw) {
 #pragma unroll
-                for (int d = 0; d < 6; ++d) P.raw[(int64_t)(1 + d) * n + i] = y[d];
+                for (int d = 0; d < 6; ++d) P.raw[(int64_t)(1 + d) * n + qi] = y[d];
             }
         }
         qhead = (qhead + rows) & (kQueue - 1);
         qcount -= rows;
     };
 
-    for (int k = 0; tile < P.n_tiles; ++k, tile += group_stride) {
-        const int st = k & 1;
+    for (int it = 0; tile < P.n_tiles; ++it, tile += group_stride) {
+        const int st = it & 1;
         const int64_t base = tile * kTile;
         const int64_t i = base + t;
         const bool in_range = i < n;
         // next tile's inputs -> other stage (its previous contents were consumed a tile ago)
         const int64_t next = tile + group_stride;
-        if (t == 0 && next < P.n_tiles && tile_full_tma(next)) {
-            fence_proxy_async();
-            mbar_expect_tx(&S.bar_in[g][st ^ 1], kStageBytes);
-            const float* src[6] = {P.in.ox, P.in.oy, P.in.dx, P.in.dy, P.in.dz, P.in.lambda_nm};
-            for (int a = 0; a < 6; ++a)
-                tma_bulk_g2s(G.stage[st ^ 1][a], src[a] + next * kTile, kTile * 4, &S.bar_in[g][st ^ 1]);
-        }
-        float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, wz = 1.f, lam = 550.f;
+        if (t == 0 && next < P.n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
+        float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
         if (tile_full_tma(tile)) {
             mbar_wait(&S.bar_in[g][st], in_phase[st]);
             in_phase[st] ^= 1u;
-            px = G.stage[st][0][t]; py = G.stage[st][1][t];
-            wx = G.stage[st][2][t]; wy = G.stage[st][3][t];
-            wz = G.stage[st][4][t]; lam = G.stage[st][5][t];
+            px = Gs.stage[st][0][t]; py = Gs.stage[st][1][t];
+            wx = Gs.stage[st][2][t]; wy = Gs.stage[st][3][t]; lam = Gs.stage[st][4][t];
         } else if (in_range) {
-            px = P.in.ox[i]; py = P.in.oy[i]; wx = P.in.dx[i]; wy = P.in.dy[i]; wz = P.in.dz[i]; lam = P.in.lambda_nm[i];
+            px = P.in.ox[i]; py = P.in.oy[i]; wx = P.in.dx[i]; wy = P.in.dy[i]; lam = P.in.lambda_nm[i];
         }
-        (void)wz;
-        // ---- canonicalise: rotate p onto +x, reflect so w'_y >= 0 ----
-        const float r = sqrtf(px * px + py * py);
-        float c, s;
-        if (r > 0.f) { const float ir = 1.f / r; c = px * ir; s = py * ir; }
-        else {
-            const float tt = sqrtf(wx * wx + wy * wy);
-            if (tt > 0.f) { c = wx / tt; s = wy / tt; } else { c = 1.f; s = 0.f; }
-        }
-        const float wpx = c * wx + s * wy;
-        float wpy = -s * wx + c * wy;
-        const bool flip = wpy < 0.f;
-        if (flip) wpy = -wpy;
-        float x[4] = {r, wpx, wpy, lam};
-#pragma unroll
-        for (int d = 0; d < 4; ++d)
-            x[d] = fminf(fmaxf((x[d] - P.mp.in_lo[d]) * P.mp.in_scale[d] - 1.f, -1.f), 1.f);
-        // ---- classifier g: 4 -> 32 -> 32 -> 1 --------------------------------------------
-        store_input(G.a, t, x);
+        const Canon k = canonicalise(P.mp, px, py, wx, wy, lam);
+        // ---- classifier g: 4 -> 32 -> 32 -> 1 ------------------------------
+        store_input(arow, k.x);
         fence_proxy_async();
-        run_layer(P.lay.cls_w[0], 1, 2, 32);
-        hidden_epilogue(bias + P.lay.cls_b[0]);
-        run_layer(P.lay.cls_w[1], 4, 4, 32);
-        hidden_epilogue(bias + P.lay.cls_b[1]);
-        run_layer(P.lay.cls_w[2], 4, 4, 16);
+        mma_layer(true, P.lay.cls_w[0], 32);
+        hidden_epilogue();
+        mma_layer(false, P.lay.cls_w[1], 32);
+        hidden_epilogue();
+        mma_layer(false, P.lay.cls_w[2], 16);
         float lg[16];
         tmem_ld16(tmem_row, lg);
-        const float logit = lg[0] + bias[P.lay.cls_b[2]];
+        const float logit = lg[0];
         const bool valid = in_range && logit >= 0.f;     // g(x) = 1 <=> logit >= 0 (A13)
         // ---- mask word + zeros for blocked rays -----------------------------------------
         const unsigned word = __ballot_sync(0xffffffffu, valid);
@@ -403,20 +423,15 @@ __global__ void __launch_bounds__(kThreads, 1) eval_map_kernel(const __grid_cons
                 }
             }
         }
-        // ---- gate: append valid rays to the group queue ---------------------------------
-        if (lane == 0) G.wcount[q] = __popc(word);
+        // ---- gate: append valid rays to the group queue (f only on the valid set)
+        if (lane == 0) Gs.wcount[q] = __popc(word);
         group_bar(g);
         int before = 0, total = 0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) { const int cw = G.wcount[w]; before += w < q ? cw : 0; total += cw; }
-        if (valid) {
-            const int e = (qhead + qcount + before + __popc(word & ((1u << lane) - 1u))) & (kQueue - 1);
-            G.qx[e][0] = x[0]; G.qx[e][1] = x[1]; G.qx[e][2] = x[2]; G.qx[e][3] = x[3];
-            G.qc[e] = c; G.qs[e] = s;
-            G.qi[e] = (int)i | (flip ? (int)0x80000000 : 0);
-        }
+        for (int w = 0; w < 4; ++w) { const int cw = Gs.wcount[w]; before += w < q ? cw : 0; total += cw; }
+        if (valid) Gs.qi[(qhead + qcount + before + __popc(word & ((1u << lane) - 1u))) & (kQueue - 1)] = (int)i;
         qcount += total;
-        if (qcount >= kTile) run_regressor(kTile);   // queue entries are published by run_layer's barrier
+        if (qcount >= kTile) run_regressor(kTile);
     }
     if (qcount > 0) run_regressor(qcount);
 
@@ -425,8 +440,25 @@ __global__ void __launch_bounds__(kThreads, 1) eval_map_kernel(const __grid_cons
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "r"(32 * kGroups));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "r"(kTmemCols));
     }
+}
+
+template <int G>
+int launch_groups(const Params& P, int sms, cudaStream_t stream) {
+    const size_t smem = sizeof(Smem<G>);
+    static int configured = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured != dev) {   // benign race: the attribute call is idempotent
+        cudaError_t e = cudaFuncSetAttribute(eval_map_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        configured = dev;
+    }
+    const int64_t groups_needed = (P.n_tiles + G - 1) / G;
+    const int grid = (int)(groups_needed < sms ? (groups_needed < 1 ? 1 : groups_needed) : sms);
+    eval_map_kernel<G><<<grid, 128 * G, smem, stream>>>(P);
+    return (int)cudaGetLastError();
 }
 
 }  // namespace
@@ -437,13 +469,6 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = sizeof(Smem) + 1024;
-    static thread_local int configured_dev = -1;
-    if (configured_dev != dev) {
-        cudaError_t e = cudaFuncSetAttribute(eval_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        configured_dev = dev;
-    }
     Params P{};
     P.in = in;
     P.out = out;
@@ -451,14 +476,18 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
     P.n = n;
     P.n_tiles = (n + kTile - 1) / kTile;
     auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
-    P.tma_ok = al(in.ox) && al(in.oy) && al(in.dx) && al(in.dy) && al(in.dz) && al(in.lambda_nm);
+    P.tma_ok = al(in.ox) && al(in.oy) && al(in.dx) && al(in.dy) && al(in.lambda_nm);
     P.lay = lay;
     P.mp = mp;
     P.wimg = (const uint8_t*)d_weights;
-    int64_t groups_needed = (P.n_tiles + kGroups - 1) / kGroups;
-    int grid = (int)(groups_needed < sms ? (groups_needed < 1 ? 1 : groups_needed) : sms);
-    eval_map_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(P);
-    return (int)cudaGetLastError();
+    static const int groups = [] {
+        const char* e = getenv("PLT_MAP_GROUPS");   // tuning knob (4, 6 or 7 tile pipelines per SM)
+        return e ? atoi(e) : 6;
+    }();
+    cudaStream_t s = (cudaStream_t)stream;
+    if (groups == 4) return launch_groups<4>(P, sms, s);
+    if (groups == 7) return launch_groups<7>(P, sms, s);
+    return launch_groups<6>(P, sms, s);
 }
 
 }  // namespace plt

@@ -44,14 +44,33 @@ struct Reader {
     }
 };
 
-void pack_operand(uint8_t* dst, const uint16_t* W, int fo, int fi, int n_pad, int k_total, bool dup_input) {
+uint16_t bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+float bf16_to_f(uint16_t h) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// Pack W (fo x fi, bf16 bits) and bias b (fo, fp32) into an N = n_pad, K = k_total operand.
+// Input layer (k_total = 16): k 0..fi-1 = W, fi..2fi-1 = W (hi/lo halves of A), 2fi, 2fi+1 =
+// bias hi/lo.  Hidden/output (k_total = 48): k 0..31 = W, 32/33 = bias hi/lo, rest 0.
+void pack_operand(uint8_t* dst, const uint16_t* W, const float* b, int fo, int fi, int n_pad, int k_total,
+                  bool input) {
     const int sbo = (k_total / 8) * 128;
+    const int kb = input ? 2 * fi : 32;
     for (int nn = 0; nn < n_pad; ++nn)
         for (int k = 0; k < k_total; ++k) {
             uint16_t v = 0;
             if (nn < fo) {
-                if (dup_input) { if (k < 2 * fi) v = W[nn * fi + (k % fi)]; }
-                else if (k < fi) v = W[nn * fi + k];
+                if (k < kb) { if (input || k < fi) v = W[nn * fi + (k % fi)]; }
+                else if (k == kb) v = bf16_rne(b[nn]);
+                else if (k == kb + 1) v = bf16_rne(b[nn] - bf16_to_f(bf16_rne(b[nn])));
             }
             const size_t off = (size_t)(nn / 8) * sbo + (k / 8) * 128 + (nn % 8) * 16 + (k % 8) * 2;
             std::memcpy(dst + off, &v, 2);
@@ -87,19 +106,12 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
     MapLayout& L = m->layout;
     uint32_t off = 0;
     auto place = [&](int n_pad, int k_total) { uint32_t o = off; off += (uint32_t)(n_pad * k_total * 2); return o; };
-    L.cls_w[0] = place(32, 16); L.cls_w[1] = place(32, 32); L.cls_w[2] = place(16, 32);
+    L.cls_w[0] = place(32, 16); L.cls_w[1] = place(32, 48); L.cls_w[2] = place(16, 48);
     L.reg_w[0] = place(32, 16);
-    for (int l = 1; l < 5; ++l) L.reg_w[l] = place(32, 32);
-    L.reg_w[5] = place(16, 32);
-    L.bias_off = off;
-    uint32_t boff = 0;
-    auto bplace = [&](int cnt) { uint32_t o = boff; boff += (uint32_t)cnt; return o; };
-    L.cls_b[0] = bplace(32); L.cls_b[1] = bplace(32); L.cls_b[2] = bplace(16);
-    for (int l = 0; l < 5; ++l) L.reg_b[l] = bplace(32);
-    L.reg_b[5] = bplace(16);
-    L.total_bytes = (off + boff * 4 + 15u) & ~15u;
+    for (int l = 1; l < 5; ++l) L.reg_w[l] = place(32, 48);
+    L.reg_w[5] = place(16, 48);
+    L.total_bytes = (off + 15u) & ~15u;
     m->image.assign(L.total_bytes, 0);
-    float* bias = reinterpret_cast<float*>(m->image.data() + L.bias_off);
 
     for (int head = 0; head < 2; ++head) {
         const int nl = head == 0 ? 3 : 6;
@@ -114,13 +126,12 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
             r.need(2 * W.size(), "weights");
             std::memcpy(W.data(), blob + r.off, 2 * W.size());
             r.off += 2 * W.size();
+            std::vector<float> b(fo);
+            for (uint32_t o = 0; o < fo; ++o) b[o] = r.get<float>("bias");
             const bool last = l + 1 == nl;
-            const int n_pad = last ? 16 : 32;
-            const int k_total = l == 0 ? 16 : 32;
             const uint32_t woff = head == 0 ? L.cls_w[l] : L.reg_w[l];
-            pack_operand(m->image.data() + woff, W.data(), (int)fo, (int)fi, n_pad, k_total, l == 0);
-            const uint32_t bo = head == 0 ? L.cls_b[l] : L.reg_b[l];
-            for (uint32_t o = 0; o < fo; ++o) bias[bo + o] = r.get<float>("bias");
+            pack_operand(m->image.data() + woff, W.data(), b.data(), (int)fo, (int)fi, last ? 16 : 32,
+                         l == 0 ? 16 : 48, l == 0);
         }
     }
     if (lens) {

@@ -61,16 +61,15 @@ struct MapDims {
     static constexpr int kRegLayers = 6;   // 4->32, 32->32 x4, 32->6
 };
 
-// Byte offsets of each packed B operand (bf16) inside the weight image.
+// Byte offsets of each packed B operand (bf16) inside the weight image.  Biases are
+// folded into the contraction: each operand carries an extra K chunk holding the
+// bf16 hi/lo split of the fp32 bias, matched by constant-one columns in A.
+//   input layer : N=32, K=16 (W | W | b_hi b_lo 0..)        -> 1024 B
+//   hidden layer: N=32, K=48 (W[32] | b_hi b_lo 0.. | 0..)   -> 3072 B
+//   output layer: N=16, K=48                                 -> 1536 B
 struct MapLayout {
-    // layer 0 (input) operands: N=32 rows, K=16 (x_hi[4], x_lo[4], 0...) -> 32*16*2 = 1024 B
-    // hidden operands:          N=32 rows, K=32                          -> 2048 B
-    // output operands:          N=16 rows, K=32                          -> 1024 B
     uint32_t cls_w[3];
     uint32_t reg_w[6];
-    uint32_t bias_off;     // f32 biases follow the bf16 operands
-    uint32_t cls_b[3];     // float index into bias block
-    uint32_t reg_b[6];
     uint32_t total_bytes;  // multiple of 16
 };
 

@@ -55,6 +55,7 @@ def compare_trace(gpu: dict, ora: dict, tol_p=TOL_P, tol_w=TOL_W, tol_i=TOL_I, a
         stats.update(max_dp=0.0, max_dw=0.0, max_dI=0.0)
     inval = ~gpu["valid"]
     stats["invalid_nonzero"] = int(sum(np.count_nonzero(gpu[k][inval]) for k in ("px", "py", "dx", "dy", "dz", "I")))
+    print("compare_trace", stats)
     if assert_ok:
         assert stats["mask_mismatch"] == 0, stats
         assert stats["max_dp"] <= tol_p, stats
