@@ -19,7 +19,7 @@ import os
 __all__ = ["load", "PltError", "Lens", "Map", "trace_rays", "eval_map", "splat_sensor", "film_resolve",
            "alloc_hits", "rays_to_device", "FORWARD", "BACKWARD", "FP32", "FP64", "LIB_PATH"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libplt.so")
+LIB_PATH = os.environ.get("PLT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libplt.so")
 FORWARD, BACKWARD = 0, 1
 FP32, FP64 = 0, 1
 

@@ -31,27 +31,30 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None) -> str:
+    """Build libplt.so.  `defines`/`out` are for developer instrumentation builds only."""
+    obj_dir, out_path = OBJ, OUT
+    if defines:
+        tag = "_".join(d.lower() for d in defines)
+        obj_dir = os.path.join(HERE, "build_" + tag)
+        out_path = out or os.path.join(HERE, "libplt_" + tag + ".so")
+    os.makedirs(obj_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(HERE, "..", "include", "plt.h")]
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src + ".o")
+        o = os.path.join(obj_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s, *hdrs]):
             extra = ["-Xptxas", "-v"] if verbose and src.endswith(".cu") else []
-            cmd = [NVCC, *COMMON, *extra, "-c", s, "-o", o]
-            if src.endswith(".cpp"):
-                cmd = [NVCC, *COMMON, "-x", "cu", "-c", s, "-o", o] if False else [NVCC, *COMMON, "-c", s, "-o", o]
+            cmd = [NVCC, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
             subprocess.check_call(cmd)
-    if force or _stale(OUT, objs):
-        # version script: export only the plt_* C ABI
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs,
+    if force or _stale(out_path, objs):
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out_path, *objs,
                                "-Xlinker", "--exclude-libs,ALL"])
-    return OUT
+    return out_path
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs))

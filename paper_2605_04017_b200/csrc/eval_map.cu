@@ -7,17 +7,19 @@
 // MLP into its render kernels and replaces tanh by an approximation.
 //
 // B200 design:
-//  * one persistent CTA per SM, G independent "tile pipelines" (groups of 4 warps);
+//  * one persistent CTA per SM, G = 7 independent "tile pipelines" (groups of 4 warps);
 //    a group owns 128 rays = one M=128 tcgen05 tile, thread t of the group = row t =
 //    TMEM lane t (warp q of the group reads TMEM lanes 32q..32q+31);
 //  * every layer is tcgen05.mma.cta_group::1.kind::f16 (bf16 x bf16 -> fp32) with the
-//    activation tile A in shared memory and the weights B resident in shared memory
-//    (TMA bulk-copied once per CTA), accumulator D in TMEM (32 columns per group);
+//    activation operand A in TMEM (written by tcgen05.st; 40 columns per group), the
+//    weights B resident in shared memory (TMA bulk-copied once per CTA) and the
+//    accumulator D in TMEM (32 columns per group) -- 7 x 72 of the 512 TMEM columns;
 //  * activations are carried as a bf16 hi/lo pair (A = [h_hi | h_lo], B = W for both
 //    halves), so the contraction keeps ~16 mantissa bits; plain bf16 activations
 //    would exceed the 2e-3 output tolerance (SURVEY [B3]);
-//  * epilogue per layer: tcgen05.ld -> +bias -> tanh.approx -> split -> st.shared ->
-//    fence.proxy.async -> named barrier -> one thread issues the next MMA;
+//  * biases are folded into the contraction (a bf16 hi/lo bias column pair in B times a
+//    constant (1, 1) chunk in A); epilogue per layer: tcgen05.ld -> tanh.approx -> split
+//    -> tcgen05.st -> named barrier -> one thread issues the next layer's MMAs;
 //  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs;
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
 //    memory; the regressor only runs on full 128-row tiles of queued rays (plus one
@@ -25,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 
 #include "plt_internal.h"
 
@@ -34,15 +37,13 @@ namespace {
 
 constexpr int kTile = 128;                   // rays per tile (UMMA M)
 constexpr int kQueue = 256;                  // per-group queue capacity (ring of ray indices)
-constexpr int kAChunks = 10;                 // A row: 4 hi + 4 lo + 2 bias-ones chunks of 8 bf16
-constexpr int kARowGroupBytes = kAChunks * 128;       // SBO of the A operand
-constexpr int kATileBytes = 16 * kARowGroupBytes;     // 128 rows x 80 bf16 = 20 KB
+constexpr int kACols = 40;                   // A operand in TMEM: 80 bf16 per row = 40 columns
+                                             // (cols 0-15 hi, 16-31 lo, 32-39 bias-ones chunk)
 constexpr int kNumIn = 5;                    // staged SoA inputs: ox, oy, dx, dy, lambda (dz unused)
 constexpr int kStageBytes = kNumIn * kTile * 4;
 constexpr uint32_t kMaxImageBytes = 20480;
 
 struct GroupSmem {
-    alignas(128) uint8_t a[kATileBytes];     // activation tile (K-major, no swizzle)
     alignas(16) float stage[2][kNumIn][kTile];  // TMA-staged ray inputs
     int qi[kQueue];                          // queued valid ray indices
     int wcount[4];                           // per-warp valid counts (prefix)
@@ -159,34 +160,46 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
 __device__ __forceinline__ float bf16lo_f(uint32_t p) { return __uint_as_float(p << 16); }
 __device__ __forceinline__ float bf16hi_f(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
 
-// A-tile addressing: element (row m, k) lives at (m/8)*SBO + (k/8)*128 + (m%8)*16 + (k%8)*2.
-__device__ __forceinline__ uint32_t a_row_off(int m) {
-    return (uint32_t)((m >> 3) * kARowGroupBytes + (m & 7) * 16);
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                        uint32_t accum) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+                   "r"(v[7]) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Split 16 activations (columns c0..c0+15) into bf16 hi/lo and store them in chunks
-// c0/8, c0/8+1 (hi, K 0..31) and 4+c0/8, 5+c0/8 (lo, K 32..63) of the row.
-__device__ __forceinline__ void store_hidden16(uint8_t* row, int c0, const float (&h)[16]) {
+// A operand in TMEM (kind::f16, M = 128): row m = lane m, element k of the row in 32-bit
+// column k/2 (even k in the low half).  Hidden/output layers read K = 80: columns 0-15
+// hold bf16(h) (hi), 16-31 the bf16 residual h - hi (lo), 32-39 the constant (1, 1, 0..)
+// chunk that multiplies the folded bias hi/lo column pair of B.
+// Split 16 activations (D columns c0..c0+15) into hi/lo pairs and store them.
+__device__ __forceinline__ void store_hidden16(uint32_t a_row, int c0, const float (&h)[16]) {
+    uint32_t hi[8], lo[8];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const float x0 = h[8 * c + 2 * p], x1 = h[8 * c + 2 * p + 1];
-            hi[p] = pack_bf16(x0, x1);
-            lo[p] = pack_bf16(x0 - bf16lo_f(hi[p]), x1 - bf16hi_f(hi[p]));
-        }
-        *reinterpret_cast<uint4*>(row + (c0 / 8 + c) * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(row + (4 + c0 / 8 + c) * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    for (int p = 0; p < 8; ++p) {
+        const float x0 = h[2 * p], x1 = h[2 * p + 1];
+        hi[p] = pack_bf16(x0, x1);
+        lo[p] = pack_bf16(x0 - bf16lo_f(hi[p]), x1 - bf16hi_f(hi[p]));
     }
+    tmem_st8(a_row + c0 / 2, hi);
+    tmem_st8(a_row + 16 + c0 / 2, lo);
 }
-// Input-layer A row: chunk 0 = x_hi[4], x_lo[4]; chunk 1 = (1, 1, 0, ...) (folded bias hi/lo).
-__device__ __forceinline__ void store_input(uint8_t* row, const float (&x)[4]) {
-    const uint32_t h01 = pack_bf16(x[0], x[1]), h23 = pack_bf16(x[2], x[3]);
-    const uint32_t l01 = pack_bf16(x[0] - bf16lo_f(h01), x[1] - bf16hi_f(h01));
-    const uint32_t l23 = pack_bf16(x[2] - bf16lo_f(h23), x[3] - bf16hi_f(h23));
-    *reinterpret_cast<uint4*>(row) = make_uint4(h01, h23, l01, l23);
-    *reinterpret_cast<uint4*>(row + 128) = make_uint4(0x3F803F80u, 0u, 0u, 0u);   // bf16 1.0, 1.0
+// Input-layer A row (K = 16): x_hi[4], x_lo[4], (1, 1) folded-bias pair, zeros.
+__device__ __forceinline__ void store_input(uint32_t a_row, const float (&x)[4]) {
+    uint32_t v[8];
+    v[0] = pack_bf16(x[0], x[1]);
+    v[1] = pack_bf16(x[2], x[3]);
+    v[2] = pack_bf16(x[0] - bf16lo_f(v[0]), x[1] - bf16hi_f(v[0]));
+    v[3] = pack_bf16(x[2] - bf16lo_f(v[1]), x[3] - bf16hi_f(v[1]));
+    v[4] = 0x3F803F80u;   // bf16 (1.0, 1.0)
+    v[5] = 0u; v[6] = 0u; v[7] = 0u;
+    tmem_st8(a_row, v);
 }
 
 struct Params {
@@ -222,19 +235,18 @@ __device__ __forceinline__ Canon canonicalise(const MapParams& mp, float px, flo
     return k;
 }
 
-// Layer MMAs.  Input layer: one K=16 step (x hi/lo + bias-ones).  Hidden / output
-// layers: K = 80 of A (32 hi, 32 lo, 16 bias-ones) against B = [W | W | bias chunk]
-// stored once as K = 48 (the hi and lo halves of A reuse the same W columns).
-__device__ __forceinline__ void issue_input(uint32_t tmem_d, uint32_t a_base, uint32_t b_base) {
-    umma(tmem_d, sdesc(a_base, 128, kARowGroupBytes), sdesc(b_base, 128, 256), idesc_bf16(32), 0u);
+// Layer MMAs (A from TMEM, B = weights in shared memory).  Input layer: one K=16 step
+// (x hi/lo + bias-ones).  Hidden / output layers: K = 80 of A (32 hi, 32 lo, 16 bias-ones)
+// against B = [W | bias chunk] stored once as K = 48 (hi and lo reuse the same W columns).
+__device__ __forceinline__ void issue_input(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base) {
+    umma_ts(tmem_d, tmem_a, sdesc(b_base, 128, 256), idesc_bf16(32), 0u);
 }
-__device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t a_base, uint32_t b_base, int n_out) {
+__device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base, int n_out) {
     const uint32_t id = idesc_bf16(n_out);
 #pragma unroll
     for (int ks = 0; ks < 5; ++ks) {
         const int bk = ks < 4 ? (ks & 1) : 2;
-        umma(tmem_d, sdesc(a_base + ks * 256, 128, kARowGroupBytes), sdesc(b_base + bk * 256, 128, 768), id,
-             ks > 0 ? 1u : 0u);
+        umma_ts(tmem_d, tmem_a + 8 * ks, sdesc(b_base + bk * 256, 128, 768), id, ks > 0 ? 1u : 0u);
     }
 }
 
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const int q = warp & 3;          // TMEM lane quarter
     const int lane = tid & 31;
     GroupSmem& Gs = S.g[g];
-    constexpr uint32_t kTmemCols = G <= 4 ? 128 : 256;
+    constexpr uint32_t kTmemCols = 512;   // 32 accumulator + 40 A columns per pipeline
 
     // ---- setup: barriers, TMEM, weights -------------------------------------------------
     if (tid == 0) {
@@ -266,18 +278,19 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
                      ::"r"(smem_u32(&S.tmem_base)), "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // constant bias-ones chunks (8, 9) of every row of this group's A tile
-    {
-        uint8_t* row = Gs.a + a_row_off(t);
-        *reinterpret_cast<uint4*>(row + 8 * 128) = make_uint4(0x3F803F80u, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(row + 9 * 128) = make_uint4(0u, 0u, 0u, 0u);
-        fence_proxy_async();
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = S.tmem_base + (uint32_t)(32 * g);      // this group's 32 accumulator columns
-    const uint32_t tmem_row = tmem + ((uint32_t)(32 * q) << 16);   // + lane quarter
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;                        // this warp's lane quarter
+    const uint32_t tmem = S.tmem_base + (uint32_t)(32 * g);                    // accumulator (32 cols)
+    const uint32_t tmem_row = tmem + lane_off;
+    const uint32_t tmem_a = S.tmem_base + (uint32_t)(32 * G + kACols * g);     // A operand (40 cols)
+    const uint32_t a_row = tmem_a + lane_off;
+    {   // constant bias-ones chunk (columns 32-39) of this row's A operand
+        const uint32_t ones[8] = {0x3F803F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        tmem_st8(a_row + 32, ones);
+        tmem_st_wait();
+    }
     if (tid == 0) {
         mbar_expect_tx(&S.bar_w, P.lay.total_bytes);
         tma_bulk_g2s(S.w, P.wimg, P.lay.total_bytes, &S.bar_w);
@@ -298,8 +311,6 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         tma_bulk_g2s(Gs.stage[st][4], P.in.lambda_nm + o, kTile * 4, &S.bar_in[g][st]);
     };
 
-    uint8_t* arow = Gs.a + a_row_off(t);
-    const uint32_t a_base = smem_u32(Gs.a);
     const uint32_t w_base = smem_u32(S.w);
     uint32_t mma_phase = 0;
     uint32_t in_phase[2] = {0, 0};
@@ -308,31 +319,70 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     if (t == 0 && tile < P.n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
     mbar_wait(&S.bar_w, 0);
 
+#ifdef PLT_MAP_PROFILE
+    long long pr_bar = 0, pr_issue = 0, pr_wait = 0, pr_epi = 0, pr_ld = 0, pr_tanh = 0, pr_st = 0, pr_fence = 0;
+    long long pr_layers = 0, pr_ifence = 0, pr_immas = 0, pr_icommit = 0;
+    const long long pr_t0 = clock64();
+#define PLT_CLK(v) const long long v = clock64()
+#else
+#define PLT_CLK(v)
+#endif
     // A stored + fenced by every thread -> barrier -> one thread issues -> wait.
     auto mma_layer = [&](bool input, uint32_t b_off, int n_out) {
+        PLT_CLK(c0);
         tc_fence_before();
         group_bar(g);
+        PLT_CLK(c1);
         if (t == 0) {
             tc_fence_after();
-            if (input) issue_input(tmem, a_base, w_base + b_off);
-            else issue_hidden(tmem, a_base, w_base + b_off, n_out);
+            PLT_CLK(i0);
+            if (input) issue_input(tmem, tmem_a, w_base + b_off);
+            else issue_hidden(tmem, tmem_a, w_base + b_off, n_out);
+            PLT_CLK(i1);
             umma_commit(&S.bar_mma[g]);
+#ifdef PLT_MAP_PROFILE
+            const long long i2 = clock64();
+            pr_ifence += i0 - c1; pr_immas += i1 - i0; pr_icommit += i2 - i1;
+#endif
         }
+        PLT_CLK(c2);
         mbar_wait(&S.bar_mma[g], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
+#ifdef PLT_MAP_PROFILE
+        const long long c3 = clock64();
+        pr_bar += c1 - c0; pr_issue += c2 - c1; pr_wait += c3 - c2; ++pr_layers;
+#endif
     };
     // hidden epilogue: TMEM (bias already folded) -> tanh -> hi/lo -> A tile, in two halves
     auto hidden_epilogue = [&]() {
+        PLT_CLK(e0);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
+            PLT_CLK(h0);
             float v[16];
             tmem_ld16(tmem_row + 16 * half, v);
+            PLT_CLK(h1);
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
-            store_hidden16(arow, 16 * half, v);
+#ifdef PLT_MAP_PROFILE
+            float sink = 0.f;
+            for (int j = 0; j < 16; ++j) sink += v[j];
+            if (sink == 12345.f) v[0] += 1.f;   // force tanh completion before the next stamp
+#endif
+            PLT_CLK(h2);
+            store_hidden16(a_row, 16 * half, v);
+            PLT_CLK(h3);
+#ifdef PLT_MAP_PROFILE
+            pr_ld += h1 - h0; pr_tanh += h2 - h1; pr_st += h3 - h2;
+#endif
         }
-        fence_proxy_async();
+        PLT_CLK(f0);
+        tmem_st_wait();
+#ifdef PLT_MAP_PROFILE
+        const long long e1 = clock64();
+        pr_fence += e1 - f0; pr_epi += e1 - e0;
+#endif
     };
 
     int qhead = 0, qcount = 0;
@@ -347,8 +397,8 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             wy = __ldg(P.in.dy + qi); lam = __ldg(P.in.lambda_nm + qi);
         }
         const Canon k = canonicalise(P.mp, px, py, wx, wy, lam);
-        store_input(arow, k.x);
-        fence_proxy_async();
+        store_input(a_row, k.x);
+        tmem_st_wait();
         mma_layer(true, P.lay.reg_w[0], 32);
         hidden_epilogue();
 #pragma unroll 1
@@ -398,8 +448,8 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         }
         const Canon k = canonicalise(P.mp, px, py, wx, wy, lam);
         // ---- classifier g: 4 -> 32 -> 32 -> 1 ------------------------------
-        store_input(arow, k.x);
-        fence_proxy_async();
+        store_input(a_row, k.x);
+        tmem_st_wait();
         mma_layer(true, P.lay.cls_w[0], 32);
         hidden_epilogue();
         mma_layer(false, P.lay.cls_w[1], 32);
@@ -434,6 +484,17 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         if (qcount >= kTile) run_regressor(kTile);
     }
     if (qcount > 0) run_regressor(qcount);
+#ifdef PLT_MAP_PROFILE
+    if (blockIdx.x == 0 && (t == 0 || t == 32)) {
+        const long long tot = clock64() - pr_t0;
+        printf("PROF blk0 pipe %d t %d: total %lld layers %lld | per layer: bar %lld issue %lld wait %lld epi %lld "
+               "(ld %lld tanh %lld st %lld fence %lld) | other/layer %lld | issue: fence %lld mmas %lld commit %lld\n",
+               g, t, tot, pr_layers, pr_bar / pr_layers, pr_issue / pr_layers, pr_wait / pr_layers,
+               pr_epi / pr_layers, pr_ld / pr_layers, pr_tanh / pr_layers, pr_st / pr_layers, pr_fence / pr_layers,
+               (tot - pr_bar - pr_issue - pr_wait - pr_epi) / pr_layers, pr_ifence / pr_layers,
+               pr_immas / pr_layers, pr_icommit / pr_layers);
+    }
+#endif
 
     // ---- teardown --------------------------------------------------------------------------
     tc_fence_before();
@@ -482,12 +543,12 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
     P.wimg = (const uint8_t*)d_weights;
     static const int groups = [] {
         const char* e = getenv("PLT_MAP_GROUPS");   // tuning knob (4, 6 or 7 tile pipelines per SM)
-        return e ? atoi(e) : 6;
+        return e ? atoi(e) : 7;
     }();
     cudaStream_t s = (cudaStream_t)stream;
     if (groups == 4) return launch_groups<4>(P, sms, s);
-    if (groups == 7) return launch_groups<7>(P, sms, s);
-    return launch_groups<6>(P, sms, s);
+    if (groups == 6) return launch_groups<6>(P, sms, s);
+    return launch_groups<7>(P, sms, s);
 }
 
 }  // namespace plt

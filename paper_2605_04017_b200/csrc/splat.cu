@@ -26,47 +26,58 @@ __global__ void __launch_bounds__(kThreads) splat_kernel(plt_film_desc fd, int64
                                                          plt_hits hits, const uint8_t* __restrict__ channel,
                                                          float scale, int64_t n,
                                                          unsigned long long* dropped) {
+    constexpr int kUnroll = 2;   // rays per thread per iteration (all loads issued up front)
     __shared__ long long wsm[kThreads];
     const int lane = threadIdx.x & 31;
     const int warp0 = threadIdx.x & ~31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kUnroll;
     const double W = fd.sensor_w_mm, H = fd.sensor_h_mm;
-    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < n; base += stride) {
-        const int64_t i = base + lane;
-        long long key = -1, w = 0;
-        bool drop = false;
-        if (i < n) {
-            const uint32_t word = __ldg(hits.mask_bits + (i >> 5));
-            if ((word >> (i & 31)) & 1u) {
-                const double px = (double)__ldg(hits.px + i), py = (double)__ldg(hits.py + i);
-                const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn(px, fd.center_x_mm), W * 0.5), W),
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kUnroll + warp0 * kUnroll; base < n; base += stride) {
+        uint32_t word[kUnroll];
+        float px[kUnroll], py[kUnroll], dz[kUnroll], I[kUnroll];
+        int ch[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {      // independent loads: one memory latency per iteration
+            const int64_t i = base + 32 * u + lane;
+            const bool in = i < n;
+            word[u] = in ? __ldg(hits.mask_bits + (i >> 5)) : 0u;
+            px[u] = in ? __ldg(hits.px + i) : 0.f;
+            py[u] = in ? __ldg(hits.py + i) : 0.f;
+            dz[u] = in ? __ldg(hits.dz + i) : 0.f;
+            I[u] = in ? __ldg(hits.throughput + i) : 0.f;
+            ch[u] = (in && channel) ? (int)__ldg(channel + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            long long key = -1, w = 0;
+            bool drop = false;
+            if ((word[u] >> lane) & 1u) {
+                const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn((double)px[u], fd.center_x_mm), W * 0.5), W),
                                             (double)fd.width_px);
-                const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(H * 0.5, __dsub_rn(py, fd.center_y_mm)), H),
+                const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(H * 0.5, __dsub_rn((double)py[u], fd.center_y_mm)), H),
                                             (double)fd.height_px);
                 const double fxf = floor(fx), fyf = floor(fy);
-                const int c = channel ? (int)__ldg(channel + i) : 0;
                 if (fxf >= 0.0 && fxf < (double)fd.width_px && fyf >= 0.0 && fyf < (double)fd.height_px &&
-                    c < fd.channels) {
-                    key = ((long long)c * fd.height_px + (long long)fyf) * fd.width_px + (long long)fxf;
-                    const double I = (double)__ldg(hits.throughput + i);
-                    const double dz = fabs((double)__ldg(hits.dz + i));
-                    w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn(I, dz), (double)scale), 4294967296.0));
+                    ch[u] < fd.channels) {
+                    key = ((long long)ch[u] * fd.height_px + (long long)fyf) * fd.width_px + (long long)fxf;
+                    w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn((double)I[u], fabs((double)dz[u])), (double)scale),
+                                                 4294967296.0));
                 } else {
                     drop = true;
                 }
             }
+            wsm[threadIdx.x] = w;
+            __syncwarp();
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (key >= 0 && lane == __ffs(peers) - 1) {
+                long long sum = 0;
+                for (unsigned p = peers; p; p &= p - 1) sum += wsm[warp0 + __ffs(p) - 1];
+                atomicAdd(reinterpret_cast<unsigned long long*>(film + key), (unsigned long long)sum);
+            }
+            const unsigned dm = __ballot_sync(0xffffffffu, drop);
+            if (dropped && lane == 0 && dm) atomicAdd(dropped, (unsigned long long)__popc(dm));
+            __syncwarp();
         }
-        wsm[threadIdx.x] = w;
-        __syncwarp();
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        if (key >= 0 && lane == __ffs(peers) - 1) {
-            long long sum = 0;
-            for (unsigned p = peers; p; p &= p - 1) sum += wsm[warp0 + __ffs(p) - 1];
-            atomicAdd(reinterpret_cast<unsigned long long*>(film + key), (unsigned long long)sum);
-        }
-        const unsigned dm = __ballot_sync(0xffffffffu, drop);
-        if (dropped && lane == 0 && dm) atomicAdd(dropped, (unsigned long long)__popc(dm));
-        __syncwarp();
     }
 }
 
@@ -83,7 +94,7 @@ int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, c
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t blocks = (n + kThreads - 1) / kThreads;
+    int64_t blocks = (n + 2 * kThreads - 1) / (2 * kThreads);
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     if (blocks < 1) blocks = 1;
     splat_kernel<<<(int)blocks, kThreads, 0, (cudaStream_t)stream>>>(fd, film, hits, channel, scale, n, dropped);

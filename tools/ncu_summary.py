@@ -24,10 +24,12 @@ def raw(rep):
     return rows[0], rows[1], rows[2:]
 
 
-def main(rep, top=25):
+def main(rep, top=25, which=None):
     h, u, data = raw(rep)
-    for r in data[:1]:
-        print("kernel:", r[h.index("Kernel Name")][:100])
+    for kidx, r in enumerate(data):
+        if which is not None and kidx != which:
+            continue
+        print("kernel[%d]:" % kidx, r[h.index("Kernel Name")][:100])
         for k in KEYS:
             if k in h:
                 print(f"  {k:70s} {r[h.index(k)]:>16s} {u[h.index(k)]}")
@@ -39,23 +41,38 @@ def main(rep, top=25):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hh = rows[1]
-    d = rows[2:]
-    si, src, ex = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source"), hh.index("Instructions Executed")
-    tot = sum(float(x[si] or 0) for x in d)
-    print(f"  top stall sites (of {tot:.0f} samples):")
-    for x in sorted(d, key=lambda x: -float(x[si] or 0))[:top]:
-        print(f"   {float(x[si] or 0) / tot * 100:5.1f}%  {x[src].strip()[:80]}")
-    c = Counter()
-    for x in d:
-        t = x[src].strip().split()
-        if not t:
+    # split into per-kernel sections (each starts with a "Kernel Name" row then a header row)
+    sections, cur = [], None
+    for row in rows:
+        if row and row[0] == "Kernel Name":
+            cur = {"name": row[1] if len(row) > 1 else "", "rows": []}
+            sections.append(cur)
+        elif cur is not None:
+            cur["rows"].append(row)
+    seen = set()
+    for sidx, sec in enumerate(sections):
+        if which is not None and sidx != which:
             continue
-        op = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
-        c[op.split(".")[0]] += float(x[ex] or 0)
-    tot_i = sum(c.values())
-    print("  instruction mix:", ", ".join(f"{k}={v / tot_i * 100:.1f}%" for k, v in c.most_common(16)))
+        if sec["name"] in seen and which is None:
+            continue
+        seen.add(sec["name"])
+        hh, d = sec["rows"][0], sec["rows"][1:]
+        si, src, ex = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source"), hh.index("Instructions Executed")
+        tot = sum(float(x[si] or 0) for x in d) or 1.0
+        print(f"== {sec['name'][:80]}: top stall sites (of {tot:.0f} samples):")
+        for x in sorted(d, key=lambda x: -float(x[si] or 0))[:top]:
+            print(f"   {float(x[si] or 0) / tot * 100:5.1f}%  {x[src].strip()[:80]}")
+        c = Counter()
+        for x in d:
+            t = x[src].strip().split()
+            if not t:
+                continue
+            op = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
+            c[op.split(".")[0]] += float(x[ex] or 0)
+        tot_i = sum(c.values()) or 1.0
+        print("  instruction mix:", ", ".join(f"{k}={v / tot_i * 100:.1f}%" for k, v in c.most_common(16)))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25,
+         int(sys.argv[3]) if len(sys.argv) > 3 else None)
