@@ -352,12 +352,14 @@ template <typename T>
 void fill_step(Step<T>* st, const Surface& s, int kind, int is_R, int dir, const Glass& far) {
     st->z = (T)s.z;
     st->R = (T)s.R;
+    st->twoR = (T)(2.0 * s.R);
     st->invR = s.R == 0.0 ? (T)0 : (T)(1.0 / s.R);
-    st->a = (T)s.a;
     st->a2 = (T)(s.a * s.a);
+    st->band_a = (T)(2.0 * s.a * kTraceBandEdge);
+    st->sdir = (T)dir;
     st->kind = kind;
     st->is_R = is_R;
-    st->dir = dir;
+    st->pad = 0;
     double g[6];
     far.device_form(&st->gform, g);
     for (int i = 0; i < 6; ++i) st->g[i] = (T)g[i];
@@ -408,9 +410,15 @@ std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, 
     const double z_out = dir == PLT_FORWARD ? L.sensor_z : zS - L.opts.backward_exit_z_mm;
     const bool rect = dir == PLT_FORWARD && L.opts.sensor_w_mm > 0 && L.opts.sensor_h_mm > 0;
     const double H = L.opts.housing_radius_mm;
+    // block-level compaction point: right after the (first) stop crossing, else mid-path
+    int split = ns / 2;
+    for (int i = 0; i < ns; ++i)
+        if (cp->pf.st[i].kind == kStop) { if (i + 1 < ns && i > 0) split = i + 1; break; }
     auto fill_prog = [&](auto& P) {
         using T = std::remove_reference_t<decltype(P.z_out)>;
         P.n_steps = ns;
+        P.split = split;
+        P.band_h = (T)(2.0 * H * kTraceBandEdge);
         P.flip = dir == PLT_BACKWARD;
         P.has_rect = rect;
         P.has_housing = H > 0;

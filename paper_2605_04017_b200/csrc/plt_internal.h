@@ -21,31 +21,39 @@ constexpr int kMaxSteps = 40;   // two-bounce ghosts of a 12-surface lens + 3 st
 enum StepKind : int { kSphere = 0, kPlane = 1, kStop = 2 };
 enum GlassForm : int { kCauchyForm = 0, kSellmeier = 1 };
 
+// Guard band of the float32 trace on geometric edges (mm); see trace.cu.
+constexpr double kTraceBandEdge = 5e-4;
+
 template <typename T>
 struct Step {
     T z;        // vertex z in the traversal frame
     T R;        // signed radius (0 for planes / stop)
+    T twoR;     // 2R
     T invR;     // 1/R (0 for planes)
     T a2;       // clear semi-aperture squared
-    T a;        // clear semi-aperture (guard-band scaling)
+    T band_a;   // 2 a kTraceBandEdge: guard band on rho^2 - a^2
+    T sdir;     // expected sign of w_z when the ray meets this surface (+1 / -1)
     T g[6];     // glass on the far side: Cauchy form n = g0 + g1 u + g2 u^2 (u = 1/lambda_um^2)
                 // or Sellmeier B1..B3, C1..C3 (um^2)
     int kind;   // StepKind
     int is_R;   // interaction: 0 = T (refract), 1 = R (reflect)
-    int dir;    // expected sign of w_z when the ray meets this surface
     int gform;  // GlassForm
+    int pad;
 };
 
 template <typename T>
 struct Program {
     int n_steps;
+    int split;        // block-level compaction of surviving rays before this step
     int flip;         // 1 for PLT_BACKWARD: input dz and plane are mirrored, output dz negated
     int has_rect;
     int has_housing;
+    int pad;
     T z_out;          // output plane in the traversal frame
     T z_mirror;       // zS for the backward frame (z' = zS - z)
     T housing;        // housing radius
     T housing2;
+    T band_h;         // 2 H kTraceBandEdge
     T rect_hw, rect_hh, rect_cx, rect_cy;
     Step<T> st[kMaxSteps];
 };
