@@ -79,12 +79,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t phase) {
         "}\n" : "=r"(ok) : "r"(smem_u32(b)), "r"(phase) : "memory");
     return ok != 0;
 }
-// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.  The
+// clock is only consulted every 64 polls so the spin costs few issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
     if (mbar_try_wait(b, phase)) return;
     const long long t0 = clock64();
-    while (!mbar_try_wait(b, phase)) {
-        if (clock64() - t0 > (1ll << 34)) __trap();   // ~9 s at 1.9 GHz
+    for (uint32_t k = 1;; ++k) {
+        if (mbar_try_wait(b, phase)) return;
+        if ((k & 63u) == 0 && clock64() - t0 > (1ll << 34)) __trap();   // ~9 s at 1.9 GHz
     }
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -178,14 +180,24 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // column k/2 (even k in the low half).  Hidden/output layers read K = 80: columns 0-15
 // hold bf16(h) (hi), 16-31 the bf16 residual h - hi (lo), 32-39 the constant (1, 1, 0..)
 // chunk that multiplies the folded bias hi/lo column pair of B.
+// bf16 pair packing by truncation: hi = top 16 bits of each float (exactly a bf16), one PRMT
+// per pair; the residual lo = x - hi is exact in fp32 and rounded once to bf16, so
+// hi + lo carries ~16 mantissa bits exactly as with a rounded hi.
+__device__ __forceinline__ uint32_t pack_hi_trunc(float x0, float x1) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(d) : "r"(__float_as_uint(x0)), "r"(__float_as_uint(x1)));
+    return d;
+}
+__device__ __forceinline__ float hi_trunc_f(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u); }
+
 // Split 16 activations (D columns c0..c0+15) into hi/lo pairs and store them.
 __device__ __forceinline__ void store_hidden16(uint32_t a_row, int c0, const float (&h)[16]) {
     uint32_t hi[8], lo[8];
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
         const float x0 = h[2 * p], x1 = h[2 * p + 1];
-        hi[p] = pack_bf16(x0, x1);
-        lo[p] = pack_bf16(x0 - bf16lo_f(hi[p]), x1 - bf16hi_f(hi[p]));
+        hi[p] = pack_hi_trunc(x0, x1);
+        lo[p] = pack_bf16(x0 - hi_trunc_f(x0), x1 - hi_trunc_f(x1));
     }
     tmem_st8(a_row + c0 / 2, hi);
     tmem_st8(a_row + 16 + c0 / 2, lo);
@@ -193,10 +205,10 @@ __device__ __forceinline__ void store_hidden16(uint32_t a_row, int c0, const flo
 // Input-layer A row (K = 16): x_hi[4], x_lo[4], (1, 1) folded-bias pair, zeros.
 __device__ __forceinline__ void store_input(uint32_t a_row, const float (&x)[4]) {
     uint32_t v[8];
-    v[0] = pack_bf16(x[0], x[1]);
-    v[1] = pack_bf16(x[2], x[3]);
-    v[2] = pack_bf16(x[0] - bf16lo_f(v[0]), x[1] - bf16hi_f(v[0]));
-    v[3] = pack_bf16(x[2] - bf16lo_f(v[1]), x[3] - bf16hi_f(v[1]));
+    v[0] = pack_hi_trunc(x[0], x[1]);
+    v[1] = pack_hi_trunc(x[2], x[3]);
+    v[2] = pack_bf16(x[0] - hi_trunc_f(x[0]), x[1] - hi_trunc_f(x[1]));
+    v[3] = pack_bf16(x[2] - hi_trunc_f(x[2]), x[3] - hi_trunc_f(x[3]));
     v[4] = 0x3F803F80u;   // bf16 (1.0, 1.0)
     v[5] = 0u; v[6] = 0u; v[7] = 0u;
     tmem_st8(a_row, v);
