@@ -40,6 +40,21 @@ TANH_PER_RAY_CLS, TANH_PER_RAY_REG = 64, 160      # 2x32 classifier, 5x32 regres
 MAC_CLS, MAC_REG = 4 * 32 + 32 * 32 + 32, 4 * 32 + 4 * 32 * 32 + 32 * 6
 IO_BYTES_PER_RAY = 6 * 4 + 6 * 4 + 1.0 / 8        # SoA in + SoA out + 1 mask bit
 MUFU_PER_CLK_PER_SM = 16                           # B200 nominal SFU rate (DESIGN.md roofline)
+FP32_LANES_PER_SM = 128                            # FFMA lanes per SM (DESIGN.md roofline)
+# Algorithmic FP32 FLOPs of the exact trace (counted from the O1-O8
+# formulas, add/mul/div/sqrt = 1 FLOP): per spherical interaction step 77, per stop 13,
+# output plane 6, input normalisation 9; weighted by the measured survival fraction at
+# each step of the C2 path (rays stop costing work once vignetted).
+TRACE_FLOPS_STEP, TRACE_FLOPS_STOP, TRACE_FLOPS_OUT, TRACE_FLOPS_INIT = 77, 13, 6, 9
+C2_ALIVE_BEFORE_STEP = (1.0, 0.837, 0.837, 0.781, 0.781, 0.738, 0.614, 0.561, 0.498, 0.441, 0.388)  # stop = 6th
+C2_ALIVE_AT_OUTPUT = 0.371
+
+
+def trace_flops_per_ray_c2() -> float:
+    f = TRACE_FLOPS_INIT + C2_ALIVE_AT_OUTPUT * TRACE_FLOPS_OUT
+    for k, a in enumerate(C2_ALIVE_BEFORE_STEP):
+        f += a * (TRACE_FLOPS_STOP if k == 5 else TRACE_FLOPS_STEP)
+    return f
 
 
 def load_peaks():
@@ -310,6 +325,8 @@ def run_plt(args, ws, rank, local):
     mufu_peak = MUFU_PER_CLK_PER_SM * 148 * sm_max * 1e6 / 1e9       # G tanh/s
     map_ach = tanh_per_launch / per_step["eval_map"] / 1e9
     flops_map = 2.0 * n * (MAC_CLS + MAC_REG * v_map)
+    fp32_peak = FP32_LANES_PER_SM * 2 * 148 * sm_max * 1e6 / 1e12         # TFLOP/s
+    trace_tflops = n * trace_flops_per_ray_c2() / per_step["trace_rays"] / 1e12
     trace_bytes = n * IO_BYTES_PER_RAY
     kernels = {
         "eval_map": {"ms": per_step["eval_map"] * 1e3, "M_rays_s": n / per_step["eval_map"] / 1e6,
@@ -322,10 +339,12 @@ def run_plt(args, ws, rank, local):
                      "hbm_GBs": trace_bytes / per_step["eval_map"] / 1e9},
         "trace_rays": {"ms": per_step["trace_rays"] * 1e3, "M_rays_s": n / per_step["trace_rays"] / 1e6,
                        "valid_frac": v_trace,
-                       "roofline": {"bound": "hbm", "achieved": trace_bytes / per_step["trace_rays"] / 1e9,
-                                    "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
-                                    "frac": trace_bytes / per_step["trace_rays"] / 1e9 / float(peaks["hbm_gbs"]),
-                                    "note": "instruction-issue bound in practice (DESIGN.md)"}},
+                       "roofline": {"bound": "alu", "achieved": trace_tflops, "peak": fp32_peak,
+                                    "unit": "TFLOP/s", "frac": trace_tflops / fp32_peak,
+                                    "peak_source": "128 FP32 lanes x 2 x 148 SMs x sm_max_mhz (DESIGN.md)",
+                                    "flops_per_ray": trace_flops_per_ray_c2()},
+                       "hbm_GBs": trace_bytes / per_step["trace_rays"] / 1e9,
+                       "hbm_frac": trace_bytes / per_step["trace_rays"] / 1e9 / float(peaks["hbm_gbs"])},
         "splat_sensor": {"ms": per_step["splat_sensor"] * 1e3},
         "film_allreduce": {"ms": per_step["film_allreduce"] * 1e3},
     }
