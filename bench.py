@@ -66,48 +66,66 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    """SM clock + throttle reasons sampled every ~5 ms (NVML) while the timed region runs.
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    Samples are kept only between mark_start() and mark_stop() (host wall clock around the
+    device-timed region), so the reported median is the clock under load."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
+        import threading
         self.index = index
-        self.proc = None
+        self.samples = []          # (t, sm_mhz, reasons_mask)
+        self.t0 = self.t1 = None
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.ok = False
+        self.max_mhz = None
+
+    def _run(self, h, nv):
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            return
+        self.thread = threading.Thread(target=self._run, args=(h, nv), daemon=True)
+        self.thread.start()
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                smax.append(float(f[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_ev.set()
+        self.thread.join(timeout=2)
+        inside = [x for x in self.samples if self.t0 is not None and self.t0 <= x[0] <= (self.t1 or 1e30)]
+        use = inside or self.samples
+        reasons = sorted({k for _, _, rs in use for k, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median([x[1] for x in use])) if use else None,
+                "sm_max_mhz": float(self.max_mhz), "reasons": reasons, "samples": len(inside)}
 
 
 # ---------------------------------------------------------------------------------------
@@ -145,7 +163,8 @@ def oracle_step(olens, blob, rays, pid, threads):
 
 
 def cpu_baseline(target_s: float = 12.0):
-    """Oracle throughput on this host's cores over a bounded sample of the C2 workload."""
+    """Oracle throughput on this host's cores over a bounded sample of the C2 workload:
+    consecutive 2^20-ray chunks of the C2 batch until ~target_s seconds of CPU work."""
     import oracle
     from plt_inputs import configs as C
     from plt_inputs import rays as R
@@ -154,18 +173,18 @@ def cpu_baseline(target_s: float = 12.0):
     pid = 1 << olens.n_optical
     blob = C.map_blob("C2", pid)
     threads = oracle.host_threads()
-    n = 1 << 14
-    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
-    t0 = time.perf_counter()
-    oracle_step(olens, blob, rays, pid, threads)
-    dt = time.perf_counter() - t0
-    n2 = int(min(1 << 22, max(1 << 14, n * target_s / max(dt, 1e-3))))
-    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n2)
-    t0 = time.perf_counter()
-    oracle_step(olens, blob, rays, pid, threads)
-    dt = time.perf_counter() - t0
-    return {"value": n2 / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"first {n2} rays of C2 (dgauss50, all-T trace + map + splat, float64), {dt:.1f} s"}
+    chunk = 1 << 20
+    done, busy, c = 0, 0.0, 0
+    while busy < target_s and c < 64:
+        rays = R.gen_rays(cfg["law"], cfg["seed"], c * chunk, chunk)
+        t0 = time.perf_counter()
+        oracle_step(olens, blob, rays, pid, threads)
+        busy += time.perf_counter() - t0
+        done += chunk
+        c += 1
+    return {"value": done / busy / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {done} rays of the C2 batch ({c} chunks of 2^20; all-T trace + map + splat "
+                      f"in float64), {busy:.1f} s of CPU time"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -259,17 +278,18 @@ def run_plt(args, ws, rank, local):
 
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.3)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark_start()
     t0.record(stream)
     for k in range(args.steps):
         step(evs[k])
     t1.record(stream)
     torch.cuda.synchronize()
+    sampler.mark_stop()
     if dist is not None:
         dist.barrier()
     clocks = sampler.stop()
@@ -378,7 +398,7 @@ def run_plt(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["plt", "reference"], default="plt")
     ap.add_argument("--rays", type=int, default=1 << 24, help="rays per GPU per step")

@@ -32,6 +32,10 @@ __global__ void __launch_bounds__(kThreads) splat_kernel(plt_film_desc fd, int64
     const int warp0 = threadIdx.x & ~31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kUnroll;
     const double W = fd.sensor_w_mm, H = fd.sensor_h_mm;
+    constexpr float kGuard = 2e-3f;
+    const float cxf = (float)fd.center_x_mm, cyf = (float)fd.center_y_mm;
+    const float hwf = (float)(0.5 * W), hhf = (float)(0.5 * H);
+    const float sxf = (float)(fd.width_px / W), syf = (float)(fd.height_px / H);
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kUnroll + warp0 * kUnroll; base < n; base += stride) {
         uint32_t word[kUnroll];
         float px[kUnroll], py[kUnroll], dz[kUnroll], I[kUnroll];
@@ -52,11 +56,19 @@ __global__ void __launch_bounds__(kThreads) splat_kernel(plt_film_desc fd, int64
             long long key = -1, w = 0;
             bool drop = false;
             if ((word[u] >> lane) & 1u) {
-                const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn((double)px[u], fd.center_x_mm), W * 0.5), W),
-                                            (double)fd.width_px);
-                const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(H * 0.5, __dsub_rn((double)py[u], fd.center_y_mm)), H),
-                                            (double)fd.height_px);
-                const double fxf = floor(fx), fyf = floor(fy);
+                // Pixel coordinate: fp32 estimate first.  Its error is < 1e-3 px for any
+                // film below 10^5 px, so when it lies more than kGuard from an integer its
+                // floor equals the floor of the exact double expression of O11; only rays
+                // near a pixel edge evaluate the double expression (bit-exact film).
+                float fxs = (px[u] - cxf + hwf) * sxf, fys = (hhf - (py[u] - cyf)) * syf;
+                double fxf = floorf(fxs), fyf = floorf(fys);
+                if (fabsf(fxs - rintf(fxs)) < kGuard || fabsf(fys - rintf(fys)) < kGuard) {
+                    const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn((double)px[u], fd.center_x_mm), W * 0.5), W),
+                                                (double)fd.width_px);
+                    const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(H * 0.5, __dsub_rn((double)py[u], fd.center_y_mm)), H),
+                                                (double)fd.height_px);
+                    fxf = floor(fx); fyf = floor(fy);
+                }
                 if (fxf >= 0.0 && fxf < (double)fd.width_px && fyf >= 0.0 && fyf < (double)fd.height_px &&
                     ch[u] < fd.channels) {
                     key = ((long long)ch[u] * fd.height_px + (long long)fyf) * fd.width_px + (long long)fxf;

@@ -51,7 +51,9 @@ __global__ void bench(long long* out, int reps, int nmma, int N, int nwarps) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
     // accumulators: warp w uses columns [w*N, w*N+N) when it fits, A (TS) lives at column 448
-    const uint32_t d = tbase + (uint32_t)((warp * N) % 448);
+    // accumulator columns must stay inside [0, 448): warps share columns when they do not fit
+    // (the results are garbage but the timing is what we measure)
+    const uint32_t d = tbase + (uint32_t)(N <= 448 / 14 ? warp * N : (warp * N) % (448 - N + 1));
     const uint32_t a_t = tbase + 448;
     const uint64_t a_s = sdesc(smem_u32(A), 128, 256);
     const uint64_t b_s = sdesc(smem_u32(B), 128, 256);
@@ -87,7 +89,6 @@ int main() {
     for (int ts = 1; ts >= 0; --ts)
         for (int N : {16, 32, 64, 128, 256})
             for (int w : {1, 2, 4, 8, 14}) {
-                if (w * N > 448 && N <= 32) continue;
                 if (ts) bench<true><<<1, 512, 16384>>>(d_out, reps, nmma, N, w);
                 else bench<false><<<1, 512, 16384>>>(d_out, reps, nmma, N, w);
                 cudaError_t e = cudaDeviceSynchronize();
