@@ -262,6 +262,33 @@ __device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t tmem_a, u
     }
 }
 
+// Last hidden layer + fp32 output layer: h = tanh(D) from TMEM, y[o] = b[o] + sum_j W[o][j] h[j]
+// (weights broadcast from shared memory) -- no MMA round for the 1- or 6-wide output.
+template <int NOUT>
+__device__ __forceinline__ void output_epilogue(uint32_t tmem_row, const float* W, const float* b, float (&y)[NOUT]) {
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) y[o] = b[o];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        float v[16];
+        tmem_ld16(tmem_row + 16 * half, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+            const float4* w4 = reinterpret_cast<const float4*>(W + o * 32 + 16 * half);
+            float acc = y[o];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 w = w4[q4];
+                acc = fmaf(w.x, v[4 * q4], acc); acc = fmaf(w.y, v[4 * q4 + 1], acc);
+                acc = fmaf(w.z, v[4 * q4 + 2], acc); acc = fmaf(w.w, v[4 * q4 + 3], acc);
+            }
+            y[o] = acc;
+        }
+    }
+}
+
 template <int G>
 __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_constant__ Params P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -366,7 +393,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         pr_bar += c1 - c0; pr_issue += c2 - c1; pr_wait += c3 - c2; ++pr_layers;
 #endif
     };
-    // hidden epilogue: TMEM (bias already folded) -> tanh -> hi/lo -> A tile, in two halves
+    // hidden epilogue: TMEM (bias already folded) -> tanh -> hi/lo -> A operand, in two halves
     auto hidden_epilogue = [&]() {
         PLT_CLK(e0);
 #pragma unroll
@@ -396,6 +423,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         pr_fence += e1 - f0; pr_epi += e1 - e0;
 #endif
     };
+    const float* outw = reinterpret_cast<const float*>(S.w + P.lay.out_off);
 
     int qhead = 0, qcount = 0;
     // regressor over queue entries [qhead, qhead + rows), rows <= 128
@@ -414,13 +442,13 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         mma_layer(true, P.lay.reg_w[0], 32);
         hidden_epilogue();
 #pragma unroll 1
-        for (int l = 1; l < 5; ++l) {
+        for (int l = 1; l < 4; ++l) {
             mma_layer(false, P.lay.reg_w[l], 32);
             hidden_epilogue();
         }
-        mma_layer(false, P.lay.reg_w[5], 16);
-        float y[16];
-        tmem_ld16(tmem_row, y);
+        mma_layer(false, P.lay.reg_w[4], 32);
+        float y[6];
+        output_epilogue<6>(tmem_row, outw + kOutRegW, outw + kOutRegB, y);
         if (live) {
             float o[6];
 #pragma unroll
@@ -465,10 +493,8 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         mma_layer(true, P.lay.cls_w[0], 32);
         hidden_epilogue();
         mma_layer(false, P.lay.cls_w[1], 32);
-        hidden_epilogue();
-        mma_layer(false, P.lay.cls_w[2], 16);
-        float lg[16];
-        tmem_ld16(tmem_row, lg);
+        float lg[1];
+        output_epilogue<1>(tmem_row, outw + kOutClsW, outw + kOutClsB, lg);
         const float logit = lg[0];
         const bool valid = in_range && logit >= 0.f;     // g(x) = 1 <=> logit >= 0 (A13)
         // ---- mask word + zeros for blocked rays -----------------------------------------

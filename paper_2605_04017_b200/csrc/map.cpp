@@ -106,12 +106,13 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
     MapLayout& L = m->layout;
     uint32_t off = 0;
     auto place = [&](int n_pad, int k_total) { uint32_t o = off; off += (uint32_t)(n_pad * k_total * 2); return o; };
-    L.cls_w[0] = place(32, 16); L.cls_w[1] = place(32, 48); L.cls_w[2] = place(16, 48);
+    L.cls_w[0] = place(32, 16); L.cls_w[1] = place(32, 48);
     L.reg_w[0] = place(32, 16);
     for (int l = 1; l < 5; ++l) L.reg_w[l] = place(32, 48);
-    L.reg_w[5] = place(16, 48);
-    L.total_bytes = (off + 15u) & ~15u;
+    L.out_off = (off + 15u) & ~15u;
+    L.total_bytes = (L.out_off + 4u * kOutFloats + 15u) & ~15u;
     m->image.assign(L.total_bytes, 0);
+    float* outw = reinterpret_cast<float*>(m->image.data() + L.out_off);
 
     for (int head = 0; head < 2; ++head) {
         const int nl = head == 0 ? 3 : 6;
@@ -128,10 +129,17 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
             r.off += 2 * W.size();
             std::vector<float> b(fo);
             for (uint32_t o = 0; o < fo; ++o) b[o] = r.get<float>("bias");
-            const bool last = l + 1 == nl;
+            if (l + 1 == nl) {   // output layer: fp32 block
+                float* wo = outw + (head == 0 ? kOutClsW : kOutRegW);
+                float* bo = outw + (head == 0 ? kOutClsB : kOutRegB);
+                for (uint32_t o = 0; o < fo; ++o) {
+                    for (uint32_t k = 0; k < fi; ++k) wo[o * fi + k] = bf16_to_f(W[o * fi + k]);
+                    bo[o] = b[o];
+                }
+                continue;
+            }
             const uint32_t woff = head == 0 ? L.cls_w[l] : L.reg_w[l];
-            pack_operand(m->image.data() + woff, W.data(), b.data(), (int)fo, (int)fi, last ? 16 : 32,
-                         l == 0 ? 16 : 48, l == 0);
+            pack_operand(m->image.data() + woff, W.data(), b.data(), (int)fo, (int)fi, 32, l == 0 ? 16 : 48, l == 0);
         }
     }
     if (lens) {

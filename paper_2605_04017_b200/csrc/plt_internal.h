@@ -69,17 +69,21 @@ struct MapDims {
     static constexpr int kRegLayers = 6;   // 4->32, 32->32 x4, 32->6
 };
 
-// Byte offsets of each packed B operand (bf16) inside the weight image.  Biases are
-// folded into the contraction: each operand carries an extra K chunk holding the
-// bf16 hi/lo split of the fp32 bias, matched by constant-one columns in A.
+// Byte offsets of each packed B operand (bf16) inside the weight image.  Biases of the
+// MMA layers are folded into the contraction: each operand carries an extra K chunk with
+// the bf16 hi/lo split of the fp32 bias, matched by constant-one columns in A.
 //   input layer : N=32, K=16 (W | W | b_hi b_lo 0..)        -> 1024 B
 //   hidden layer: N=32, K=48 (W[32] | b_hi b_lo 0.. | 0..)   -> 3072 B
-//   output layer: N=16, K=48                                 -> 1536 B
+// The output layers (classifier 32->1, regressor 32->6) are evaluated in fp32 from the
+// last hidden activations (no MMA round): their weights (bf16 values widened) and biases
+// live in an fp32 block at `out_off`: cls W[32], cls b, pad to 4, reg W[6][32], reg b[6].
 struct MapLayout {
-    uint32_t cls_w[3];
-    uint32_t reg_w[6];
+    uint32_t cls_w[2];     // classifier input + hidden operands
+    uint32_t reg_w[5];     // regressor input + 4 hidden operands
+    uint32_t out_off;      // byte offset of the fp32 output-layer block (16-byte aligned)
     uint32_t total_bytes;  // multiple of 16
 };
+constexpr int kOutClsW = 0, kOutClsB = 32, kOutRegW = 36, kOutRegB = 36 + 192, kOutFloats = 36 + 192 + 8;
 
 struct MapParams {
     float in_lo[4], in_scale[4];   // x_hat = clamp((x - lo) * scale - 1, -1, 1), scale = 2/(hi-lo)
