@@ -144,6 +144,15 @@ def dist_setup(args):
     return ws, rank, local
 
 
+def workload_config(n: int, ws: int, pid: int) -> dict:
+    """The `config` object shared by both arms (same workload, metric and unit)."""
+    return {"workload": "C2: 50 mm double-Gauss (Kolb/pbrt stand-in), 2^24 rays per GPU, lambda U[400,700] nm, "
+                        "all-T trace + factorised map (seeded Xavier bf16 weights) + splat"
+                        + (" + NCCL film all-reduce" if ws > 1 else ""),
+            "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid, "film": "768x512 int64",
+            "l2": "inputs 403 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"}
+
+
 def make_workload(rank: int, n_per_rank: int):
     from plt_inputs import configs as C
     from plt_inputs import rays as R
@@ -213,10 +222,10 @@ def run_reference(args, ws, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "C2 dgauss50 all-T trace + factorised map + splat (bounded sample)",
-                       "rays_per_step": n, "lens": "dgauss50", "path_id": pid, "lambda_nm": [400, 700]},
+            "config": workload_config(args.rays, ws, pid),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": f"{n} rays of C2 per step (of 2^24 per GPU in the GPU arm)"},
+                             "sample": f"each step = the first {n} rays of the C2 batch (bounded sample of the "
+                                       f"2^24 rays per GPU of the GPU arm), float64 trace + map + splat"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -377,11 +386,7 @@ def run_plt(args, ws, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 trace (+f64 refine), bf16xbf16->f32 map", "data": "synthetic",
-        "config": {"workload": "C2: 50 mm double-Gauss (Kolb/pbrt stand-in), 2^24 rays per GPU, "
-                               "lambda U[400,700] nm, all-T trace + factorised map (seeded Xavier bf16 "
-                               "weights) + splat" + (" + NCCL film all-reduce" if ws > 1 else ""),
-                   "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid, "film": "768x512 int64",
-                   "l2": "inputs 403 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"},
+        "config": workload_config(n, ws, pid),
         "roofline": roof,
         "kernels": kernels,
         "e2e": {"value": ws * n / e2e_s / 1e6, "unit": UNIT,
