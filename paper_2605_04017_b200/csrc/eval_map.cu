@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
 #ifdef PLT_MAP_PROFILE
     long long pr_bar = 0, pr_issue = 0, pr_wait = 0, pr_epi = 0, pr_ld = 0, pr_tanh = 0, pr_st = 0, pr_fence = 0;
     long long pr_layers = 0, pr_ifence = 0, pr_immas = 0, pr_icommit = 0;
+    long long pr_tiles = 0, pr_in = 0, pr_outep = 0, pr_write = 0, pr_queue = 0, pr_reg = 0, pr_regs = 0, pr_gather = 0;
     const long long pr_t0 = clock64();
 #define PLT_CLK(v) const long long v = clock64()
 #else
@@ -429,6 +430,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     // regressor over queue entries [qhead, qhead + rows), rows <= 128
     auto run_regressor = [&](int rows) {
         group_bar(g);   // publish queue entries written by other threads of the group
+        PLT_CLK(g0);
         const bool live = t < rows;
         const int qi = live ? Gs.qi[(qhead + t) & (kQueue - 1)] : 0;
         float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
@@ -439,6 +441,9 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         const Canon k = canonicalise(P.mp, px, py, wx, wy, lam);
         store_input(a_row, k.x);
         tmem_st_wait();
+#ifdef PLT_MAP_PROFILE
+        pr_gather += clock64() - g0;
+#endif
         mma_layer(true, P.lay.reg_w[0], 32);
         hidden_epilogue();
 #pragma unroll 1
@@ -477,6 +482,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         // next tile's inputs -> other stage (its previous contents were consumed a tile ago)
         const int64_t next = tile + group_stride;
         if (t == 0 && next < P.n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
+        PLT_CLK(o0);
         float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
         if (tile_full_tma(tile)) {
             mbar_wait(&S.bar_in[g][st], in_phase[st]);
@@ -490,12 +496,15 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         // ---- classifier g: 4 -> 32 -> 32 -> 1 ------------------------------
         store_input(a_row, k.x);
         tmem_st_wait();
+        PLT_CLK(o1);
         mma_layer(true, P.lay.cls_w[0], 32);
         hidden_epilogue();
         mma_layer(false, P.lay.cls_w[1], 32);
+        PLT_CLK(o2);
         float lg[1];
         output_epilogue<1>(tmem_row, outw + kOutClsW, outw + kOutClsB, lg);
         const float logit = lg[0];
+        PLT_CLK(o3);
         const bool valid = in_range && logit >= 0.f;     // g(x) = 1 <=> logit >= 0 (A13)
         // ---- mask word + zeros for blocked rays -----------------------------------------
         const unsigned word = __ballot_sync(0xffffffffu, valid);
@@ -511,6 +520,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
                 }
             }
         }
+        PLT_CLK(o4);
         // ---- gate: append valid rays to the group queue (f only on the valid set)
         if (lane == 0) Gs.wcount[q] = __popc(word);
         group_bar(g);
@@ -519,7 +529,13 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         for (int w = 0; w < 4; ++w) { const int cw = Gs.wcount[w]; before += w < q ? cw : 0; total += cw; }
         if (valid) Gs.qi[(qhead + qcount + before + __popc(word & ((1u << lane) - 1u))) & (kQueue - 1)] = (int)i;
         qcount += total;
+        PLT_CLK(o5);
         if (qcount >= kTile) run_regressor(kTile);
+#ifdef PLT_MAP_PROFILE
+        const long long o6 = clock64();
+        ++pr_tiles; pr_in += o1 - o0; pr_outep += o3 - o2; pr_write += o4 - o3; pr_queue += o5 - o4;
+        if (o6 - o5 > 100) { pr_reg += o6 - o5; ++pr_regs; }
+#endif
     }
     if (qcount > 0) run_regressor(qcount);
 #ifdef PLT_MAP_PROFILE
@@ -531,6 +547,10 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
                pr_epi / pr_layers, pr_ld / pr_layers, pr_tanh / pr_layers, pr_st / pr_layers, pr_fence / pr_layers,
                (tot - pr_bar - pr_issue - pr_wait - pr_epi) / pr_layers, pr_ifence / pr_layers,
                pr_immas / pr_layers, pr_icommit / pr_layers);
+        printf("PROF tiles pipe %d t %d: tiles %lld | per tile: stage+canon+store %lld, out-epilogue %lld, "
+               "writes %lld, queue %lld | regressor runs %lld avg %lld (gather+canon %lld)\n", g, t, pr_tiles,
+               pr_in / pr_tiles, pr_outep / pr_tiles, pr_write / pr_tiles, pr_queue / pr_tiles, pr_regs,
+               pr_regs ? pr_reg / pr_regs : 0, pr_regs ? pr_gather / pr_regs : 0);
     }
 #endif
 
