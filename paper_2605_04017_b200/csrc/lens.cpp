@@ -414,6 +414,10 @@ std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, 
     int split = ns / 2;
     for (int i = 0; i < ns; ++i)
         if (cp->pf.st[i].kind == kStop) { if (i + 1 < ns && i > 0) split = i + 1; break; }
+    if (const char* e = std::getenv("PLT_TRACE_SPLIT_DELTA")) {   // developer tuning knob
+        const int v = split + std::atoi(e);
+        if (v > 0 && v < ns) split = v;
+    }
     auto fill_prog = [&](auto& P) {
         using T = std::remove_reference_t<decltype(P.z_out)>;
         P.n_steps = ns;
