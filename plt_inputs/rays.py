@@ -147,6 +147,24 @@ def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     return u.astype(np.uint16)
 
 
+def write_map_blob(path_id: int, direction: int, in_lo, in_hi, out_mid, out_half, cls_layers, reg_layers) -> bytes:
+    """Serialise a factorised map from given layers [(W float32 (out, in), b float32 (out,)), ...];
+    W is rounded to bf16 (round-to-nearest-even).  Same layout as make_map_blob."""
+    parts = [MAP_MAGIC, struct.pack("<IIQII", 1, int(direction), int(path_id), len(cls_layers), len(reg_layers))]
+    for arr, n in ((in_lo, 4), (in_hi, 4), (out_mid, 6), (out_half, 6)):
+        a = np.asarray(arr, dtype=np.float32)
+        assert a.shape == (n,)
+        parts.append(a.tobytes())
+    for layers in (cls_layers, reg_layers):
+        for W, b in layers:
+            W = np.asarray(W, dtype=np.float32)
+            b = np.asarray(b, dtype=np.float32)
+            parts.append(struct.pack("<II", W.shape[0], W.shape[1]))
+            parts.append(f32_to_bf16_bits(W).tobytes())
+            parts.append(b.tobytes())
+    return b"".join(parts)
+
+
 def make_map_blob(path_id: int, direction: int, seed: int, in_lo, in_hi, out_mid, out_half,
                   bias_range: float = 0.1) -> bytes:
     """Serialise one path's factorised map (classifier + regressor) as a blob.
