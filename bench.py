@@ -147,7 +147,7 @@ def dist_setup(args):
 def workload_config(n: int, ws: int, pid: int) -> dict:
     """The `config` object shared by both arms (same workload, metric and unit)."""
     return {"workload": "C2: 50 mm double-Gauss (Kolb/pbrt stand-in), 2^24 rays per GPU, lambda U[400,700] nm, "
-                        "all-T trace + factorised map (seeded Xavier bf16 weights) + splat"
+                        "all-T trace + factorised map (fitted weights maps/C2_0.pltmap) + splat"
                         + (" + NCCL film all-reduce" if ws > 1 else ""),
             "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid, "film": "768x512 int64",
             "l2": "inputs 403 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"}
@@ -180,7 +180,7 @@ def cpu_baseline(target_s: float = 12.0):
     cfg = C.CONFIGS["C2"]
     olens = oracle.load_lens(C.lens_text("C2"), cfg["opts"])
     pid = 1 << olens.n_optical
-    blob = C.map_blob("C2", pid)
+    blob = C.fitted_map_blob("C2")
     threads = oracle.host_threads()
     chunk = 1 << 20
     done, busy, c = 0, 0.0, 0
@@ -207,7 +207,7 @@ def run_reference(args, ws, rank):
     cfg = C.CONFIGS["C2"]
     olens = oracle.load_lens(C.lens_text("C2"), cfg["opts"])
     pid = 1 << olens.n_optical
-    blob = C.map_blob("C2", pid)
+    blob = C.fitted_map_blob("C2")
     threads = oracle.host_threads()
     n = args.ref_rays
     rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
@@ -242,7 +242,7 @@ def run_plt(args, ws, rank, local):
     cfg, rays_np = make_workload(rank, n)
     lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
     pid = lens.all_t_id()
-    m = plt.Map(C.map_blob("C2", pid), lens=lens)
+    m = plt.Map(C.fitted_map_blob("C2"), lens=lens)
     stream = torch.cuda.current_stream()
 
     # inputs resident in HBM (device-timed value); pinned host copies for e2e

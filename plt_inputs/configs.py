@@ -11,6 +11,7 @@ BFL), recorded here as a plain constant.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -115,6 +116,16 @@ def flare_rays(cfg_name: str, channel: int, start: int, count: int) -> dict:
     law = dict(cfg["law"])
     law["lam"] = cfg["channels"][channel]
     return R.gen_rays(law, cfg["seed"] * 16 + channel, start, count)
+
+
+MAPS_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "maps")
+
+
+def fitted_map_blob(cfg_name: str, path_tag: int = 0) -> bytes:
+    """A committed fitted map, maps/<cfg>_<tag>.pltmap (tag 0 = all-T), written by
+    tests/fit_map.py from float64 oracle labels (maps/README.md)."""
+    with open(os.path.join(MAPS_DIR, f"{cfg_name}_{int(path_tag)}.pltmap"), "rb") as f:
+        return f.read()
 
 
 def map_blob(cfg_name: str, path_id: int, seed: int = 1234) -> bytes:

@@ -1,12 +1,18 @@
 """Offline weight fitting of one light path's factorised map on exact-trace data
 (the paper's data collection and training).
 
-    python tools/fit_map.py --config C2 [--path <id>] [--train-rays 2^23] [--steps 6000]
-                            [--out maps/c2_allT.pltmap] [--report maps/c2_allT.json]
+    python tests/fit_map.py --config C2 [--path <id>] [--train-rays 2^24] [--steps 20000]
+                            [--out maps/C2_0.pltmap] [--report profiles/r01_fit_C2_0.json]
+
+TEST INFRASTRUCTURE (it lives under tests/ because it calls the oracle): the committed
+blobs in maps/ are inputs of parity tests and of bench.py, so — like every stored
+oracle input — they are written by a script whose labels come from the float64 ORACLE
+only (oracle.trace), never from the CUDA path.  PyTorch fits the weights
+(any device); the optional --report then measures the LIBRARY's eval_map against the
+library's exact trace on held-out rays.
 
 Data: seeded rays of the config's law (a training seed disjoint from the evaluation
-seed), labelled by the library's exact trace (plt_trace_rays; float64 mode for ghost
-paths).  Inputs and targets are reduced by the rotation/reflection symmetry of §4.1
+seeds), labelled by oracle.trace in float64.  Inputs and targets are reduced by the rotation/reflection symmetry of §4.1
 (P:310-325): x = (r, w'_x, w'_y, lambda), targets (p'_x, p'_y, w'_x, w'_y, w'_z, I) in
 the canonical frame.  Classifier 4-32-32-1 (tanh) with BCE on all rays,
 regressor 4-32^5-6 (tanh) on valid rays only with MSE on position/throughput
@@ -16,8 +22,7 @@ is compressed to a few thousand large batches here).  The trained weights are ro
 to bf16 and written as a PLTMAP01 blob; accuracy of the LIBRARY's eval_map against the
 exact trace is reported on held-out rays.
 
-This is an offline tool: PyTorch trains the weights; the product path (eval_map) is the
-tcgen05 kernel.  It does not import the oracle.
+The product path (eval_map) is the tcgen05 kernel; nothing here is on it.
 """
 from __future__ import annotations
 
@@ -28,13 +33,14 @@ import os
 import sys
 import time
 
+RAY_KEYS = ("ox", "oy", "dx", "dy", "dz", "lambda_nm")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-import paper_2605_04017_b200 as plt  # noqa: E402
+import oracle  # noqa: E402
 from plt_inputs import configs as C  # noqa: E402
 from plt_inputs import rays as R  # noqa: E402
 
@@ -45,22 +51,27 @@ def unpack_mask(words: torch.Tensor, n: int) -> torch.Tensor:
     return bits.reshape(-1)[:n].bool()
 
 
-def trace_labels(lens, pid, direction, law, seed, n, precision):
-    """Exact-trace labels for n rays (chunked through the library)."""
+def oracle_labels(olens, pid, direction, law, seed, n, device):
+    """Exact float64 labels from the oracle for rays [0, n) of the law (seeded chunks)."""
+    rays = R.gen_rays(law, seed, 0, n)
+    o = oracle.trace(olens, pid, direction, rays, threads=oracle.host_threads())
+    inp = torch.from_numpy(np.stack([rays[k] for k in RAY_KEYS], 1)).to(device)
+    out = torch.from_numpy(np.stack([o[k] for k in ("px", "py", "dx", "dy", "dz", "I")], 1)).to(device)
+    return inp, out, torch.from_numpy(o["valid"]).to(device)
+
+
+def library_labels(plt, lens, pid, direction, law, seed, n, precision):
+    """Exact-trace labels from the library (report only; chunked)."""
     chunk = 1 << 22
     xs, ys, vs = [], [], []
     for s0 in range(0, n, chunk):
         cnt = min(chunk, n - s0)
-        rays = R.gen_rays(law, seed, s0, cnt)
-        d = plt.rays_to_device(rays)
+        d = plt.rays_to_device(R.gen_rays(law, seed, s0, cnt))
         h = plt.alloc_hits(cnt)
         plt.trace_rays(lens, pid, d, h, direction=direction, precision=precision)
-        v = unpack_mask(h["mask_bits"], cnt)
-        inp = torch.stack([d["ox"], d["oy"], d["dx"], d["dy"], d["dz"], d["lambda_nm"]], 1)
-        out = torch.stack([h["px"], h["py"], h["dx"], h["dy"], h["dz"], h["throughput"]], 1)
-        xs.append(inp)
-        ys.append(out)
-        vs.append(v)
+        vs.append(unpack_mask(h["mask_bits"], cnt))
+        xs.append(torch.stack([d[k] for k in RAY_KEYS], 1))
+        ys.append(torch.stack([h[k] for k in ("px", "py", "dx", "dy", "dz", "throughput")], 1))
     return torch.cat(xs), torch.cat(ys), torch.cat(vs)
 
 
@@ -125,7 +136,7 @@ def train(model, loss_fn, X, Y, steps, batch, lr0, lr_end, log_every=1000, name=
     return model
 
 
-def flare_films(cfg_name, lens, m, pid, seed_shift=0):
+def flare_films(plt, cfg_name, lens, m, pid, seed_shift=0):
     """RGB flare films of one ghost path on the config's rays (2^20 rays per
     channel), splatted from the exact trace (float64 mode) and from the map, same rays."""
     cfg = C.CONFIGS[cfg_name]
@@ -166,10 +177,10 @@ def film_diff(img, ref, fd, bins=(1, 4, 16)):
     return out
 
 
-def flare_report(cfg_name, lens, m, pid):
+def flare_report(plt, cfg_name, lens, m, pid):
     fd = C.CONFIGS[cfg_name]["film"]
-    f = flare_films(cfg_name, lens, m, pid)
-    g = flare_films(cfg_name, lens, m, pid, seed_shift=8)   # independent rays: Monte-Carlo floor
+    f = flare_films(plt, cfg_name, lens, m, pid)
+    g = flare_films(plt, cfg_name, lens, m, pid, seed_shift=8)   # independent rays: Monte-Carlo floor
     return {"map_vs_trace_same_rays": film_diff(f["map"], f["trace"], fd),
             "trace_vs_trace_other_rays": film_diff(g["trace"], f["trace"], fd),
             "map_vs_trace_other_rays": film_diff(g["map"], f["trace"], fd)}
@@ -195,11 +206,39 @@ def model_errors(reg, cls, xh, y, valid, ymid, yhalf):
     return {"mask_agreement": float((pv == valid).float().mean()), "dp_mm": quantiles(dp), "dw": quantiles(dw)}
 
 
+def library_report(a, cfg, law, pid, blob, rep):
+    """Held-out accuracy of the LIBRARY's eval_map against the library's exact trace."""
+    import paper_2605_04017_b200 as plt
+    lens = plt.Lens(C.lens_text(a.config), **cfg["opts"])
+    prec = plt.FP32 if pid == lens.all_t_id() else plt.FP64
+    inp, out, valid = library_labels(plt, lens, pid, cfg["direction"], law, 7_000_002, a.eval_rays, prec)
+    m = plt.Map(blob, lens=lens)
+    n = inp.shape[0]
+    d = {k: inp[:, j].contiguous() for j, k in enumerate(RAY_KEYS)}
+    d["plane_z"] = law["plane_z"]
+    hm = plt.alloc_hits(n)
+    plt.eval_map(m, d, hm)
+    torch.cuda.synchronize()
+    mv = unpack_mask(hm["mask_bits"], n)
+    both = mv & valid
+    dp = torch.sqrt((hm["px"] - out[:, 0]) ** 2 + (hm["py"] - out[:, 1]) ** 2)[both]
+    dw = torch.sqrt((hm["dx"] - out[:, 2]) ** 2 + (hm["dy"] - out[:, 3]) ** 2 + (hm["dz"] - out[:, 4]) ** 2)[both]
+    dI = (hm["throughput"] - out[:, 5]).abs()[both]
+    rep["eval_map_vs_library_trace"] = {
+        "rays": n, "valid_trace": float(valid.float().mean()), "valid_map": float(mv.float().mean()),
+        "mask_agreement": float((mv == valid).float().mean()),
+        "false_valid": float((mv & ~valid).float().mean()), "false_blocked": float((~mv & valid).float().mean()),
+        "dp_mm": quantiles(dp), "dw": quantiles(dw), "dI": quantiles(dI)}
+    if "channels" in cfg:
+        rep["flare"] = flare_report(plt, a.config, lens, m, pid)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--path", type=int, default=0, help="path id (0 = all-T)")
     ap.add_argument("--train-rays", type=int, default=1 << 24)
+    ap.add_argument("--holdout-rays", type=int, default=1 << 21)
     ap.add_argument("--eval-rays", type=int, default=1 << 22)
     ap.add_argument("--steps", type=int, default=20000)
     ap.add_argument("--qat-steps", type=int, default=5000)
@@ -207,22 +246,23 @@ def main():
     ap.add_argument("--balance", choices=("paper", "none"), default="paper",
                     help="paper: valid and invalid rays weigh equally in the BCE (P:387)")
     ap.add_argument("--out", default=None)
-    ap.add_argument("--report", default=None)
+    ap.add_argument("--report", default=None, help="also measure the library (needs a GPU)")
     a = ap.parse_args()
     torch.manual_seed(0)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
     cfg = C.CONFIGS[a.config]
     law = dict(cfg["law"])
     if "channels" in cfg:
         law["lam"] = (400.0, 700.0)       # flare configs: train over the visible band
-    lens = plt.Lens(C.lens_text(a.config), **cfg["opts"])
-    pid = a.path or lens.all_t_id()
+    olens = oracle.load_lens(C.lens_text(a.config), cfg["opts"])
+    pid = a.path or oracle.all_t_id(olens.n_optical)
     direction = cfg["direction"]
-    prec = plt.FP32 if pid == lens.all_t_id() else plt.FP64
     t0 = time.time()
-    inp, out, valid = trace_labels(lens, pid, direction, law, 7_000_001, a.train_rays, prec)
+    inp, out, valid = oracle_labels(olens, pid, direction, law, 7_000_001, a.train_rays, dev)
     x, y = canonical(inp, out)
     del inp, out
-    print(f"train data: {a.train_rays} rays, valid {valid.float().mean().item():.4f}, {time.time() - t0:.1f} s")
+    print(f"train data: {a.train_rays} rays (oracle), valid {valid.float().mean().item():.4f}, "
+          f"{time.time() - t0:.1f} s", flush=True)
     lo, hi = x.min(0).values, x.max(0).values
     span = (hi - lo).clamp_min(1e-6)
     lo, hi = lo - 0.01 * span, hi + 0.01 * span
@@ -234,11 +274,11 @@ def main():
     yh = ((yv - ymid) / yhalf).float()
     del x, y, yv
 
-    cls = mlp([4, 32, 32, 1]).cuda()
-    reg = mlp([4, 32, 32, 32, 32, 32, 6]).cuda()
+    cls = mlp([4, 32, 32, 1]).to(dev)
+    reg = mlp([4, 32, 32, 32, 32, 32, 6]).to(dev)
     lbl = valid.float()[:, None]
     frac = float(lbl.mean())
-    pos_w = torch.tensor((1 - frac) / max(frac, 1e-9) if a.balance == "paper" else 1.0, device="cuda")
+    pos_w = torch.tensor((1 - frac) / max(frac, 1e-9) if a.balance == "paper" else 1.0, device=dev)
     bce = torch.nn.BCEWithLogitsLoss(pos_weight=pos_w)
     yh_mid, yh_half = ymid.float(), yhalf.float()
 
@@ -249,12 +289,13 @@ def main():
         cos = torch.nn.functional.cosine_similarity(wp, wt, dim=1).mean()
         return mse + (1.0 - cos)
     xv = xh[valid]
-    inp_e, out_e, valid_e = trace_labels(lens, pid, direction, law, 7_000_002, a.eval_rays, prec)
+    inp_e, out_e, valid_e = oracle_labels(olens, pid, direction, law, 7_000_004, a.holdout_rays, dev)
     xe, ye = canonical(inp_e, out_e)
     xeh = norm_x(xe)
-    rep = {"config": a.config, "path_id": pid, "train_rays": a.train_rays, "eval_rays": int(inp_e.shape[0]),
-           "steps": a.steps, "qat_steps": a.qat_steps, "batch": a.batch, "balance": a.balance,
-           "valid_trace": float(valid_e.float().mean())}
+    rep = {"config": a.config, "path_id": pid, "labels": "oracle (float64)", "train_rays": a.train_rays,
+           "holdout_rays": a.holdout_rays, "steps": a.steps, "qat_steps": a.qat_steps, "batch": a.batch,
+           "balance": a.balance, "train_device": dev, "valid_train": frac,
+           "valid_holdout": float(valid_e.float().mean())}
     # phase 1: fp32 weights; phase 2: weights seen through bf16 rounding (eval_map's operand type)
     for phase, steps, lr0, lr1 in (("fp32", a.steps, 3e-3, 1e-5), ("bf16-qat", a.qat_steps, 1e-5, 1e-6)):
         QLinear.quant = phase != "fp32"
@@ -265,7 +306,7 @@ def main():
             QLinear.quant = True
             rep["torch_bf16_rounded_before_qat"] = model_errors(reg, cls, xeh, ye, valid_e, ymid, yhalf)
     rep["torch_bf16_after_qat"] = model_errors(reg, cls, xeh, ye, valid_e, ymid, yhalf)
-    del xh, xv, yh, lbl, xe, ye, xeh
+    del xh, xv, yh, lbl, xe, ye, xeh, inp_e, out_e, valid_e
 
     def layers_of(m):
         return [(l.weight.detach().cpu().numpy(), l.bias.detach().cpu().numpy())
@@ -276,29 +317,8 @@ def main():
         os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
         with open(a.out, "wb") as f:
             f.write(blob)
-
-    # ---- held-out accuracy of the LIBRARY eval_map vs the exact trace
-    inp, out, valid = inp_e, out_e, valid_e
-
-    m = plt.Map(blob, lens=lens)
-    n = inp.shape[0]
-    d = {k: inp[:, j].contiguous() for j, k in enumerate(plt.RAY_KEYS)}
-    d["plane_z"] = law["plane_z"]
-    hm = plt.alloc_hits(n)
-    plt.eval_map(m, d, hm)
-    torch.cuda.synchronize()
-    mv = unpack_mask(hm["mask_bits"], n)
-    both = mv & valid
-    dp = torch.sqrt((hm["px"] - out[:, 0]) ** 2 + (hm["py"] - out[:, 1]) ** 2)[both]
-    dw = torch.sqrt((hm["dx"] - out[:, 2]) ** 2 + (hm["dy"] - out[:, 3]) ** 2 + (hm["dz"] - out[:, 4]) ** 2)[both]
-    dI = (hm["throughput"] - out[:, 5]).abs()[both]
-    rep["eval_map"] = {"valid_map": float(mv.float().mean()),
-                       "mask_agreement": float((mv == valid).float().mean()),
-                       "false_valid": float((mv & ~valid).float().mean()),
-                       "false_blocked": float((~mv & valid).float().mean()),
-                       "dp_mm": quantiles(dp), "dw": quantiles(dw), "dI": quantiles(dI)}
-    if "channels" in cfg:
-        rep["flare"] = flare_report(a.config, lens, m, pid)
+    if a.report:
+        library_report(a, cfg, law, pid, blob, rep)
     rep["seconds"] = time.time() - t0
     print(json.dumps(rep, indent=1))
     if a.report:

@@ -1,4 +1,4 @@
-"""Accuracy of the committed fitted maps (maps/*.pltmap, tools/fit_map.py) evaluated by the
+"""Accuracy of the committed fitted maps (maps/*.pltmap, tests/fit_map.py) evaluated by the
 library's eval_map kernel against the library's exact trace (itself parity-pinned to the
 oracle in test_gpu_trace.py) on held-out seeded rays: the paper's claim that the
 classifier-regressor reproduces the lens transport.  This is an

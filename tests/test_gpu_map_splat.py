@@ -96,6 +96,24 @@ def test_eval_map_backward_map_c3(gpu_lib):
     compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays, threads=oracle.host_threads()))
 
 
+@pytest.mark.parametrize("tag", [("C2", 0), ("C3", 0), ("C4_22", 65616), ("C4_59", 16404)],
+                         ids=lambda t: f"{t[0]}_{t[1]}")
+def test_eval_map_fitted_weights(gpu_lib, tag):
+    """Parity on the committed fitted maps (realistic valid fractions and weight scales; the
+    blobs come from oracle labels, tests/fit_map.py), 2^17 rays of the config's law."""
+    plt = gpu_lib
+    name, ptag = tag
+    cfg = C.CONFIGS[name]
+    blob = C.fitted_map_blob(name, ptag)
+    m = plt.Map(blob, lens=plt.Lens(C.lens_text(name), **cfg["opts"]))
+    law = dict(cfg["law"])
+    if "channels" in cfg:
+        law["lam"] = (400.0, 700.0)
+    rays = R.gen_rays(law, 41, 0, (1 << 17) + 77)
+    v = compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays, threads=oracle.host_threads()))
+    assert v > 0.005
+
+
 FILM = C.CONFIGS["C4_22"]["film"]
 
 

@@ -23,7 +23,7 @@ def main():
     rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
     lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
     pid = lens.all_t_id()
-    blob = C.map_blob("C2", pid)
+    blob = C.map_blob("C2", pid) if os.environ.get("MAP") == "random" else C.fitted_map_blob("C2")
     m = plt.Map(blob, lens=lens)
     d = plt.rays_to_device(rays)
     h = plt.alloc_hits(n)
@@ -58,7 +58,7 @@ def main():
     both = dec & o["valid"] & (g[:, 0] >= 0)
     err_logit = np.abs(g[:, 0] - o["raw"][:, 0]).max()
     err_reg = np.abs(g[both, 1:] - o["raw"][both, 1:]).max(axis=0)
-    print(f"groups={os.environ.get('PLT_MAP_GROUPS', 'default')} n={n} eval_map {ms:.3f} ms "
+    print(f"lib={os.path.basename(plt.LIB_PATH)} groups={os.environ.get('PLT_MAP_GROUPS', 'default')} n={n} eval_map {ms:.3f} ms "
           f"({n / ms / 1e6:.2f} G rays/s)  trace {tms:.3f} ms ({n / tms / 1e6:.2f} G rays/s)  "
           f"valid={o['valid'].mean():.3f} err_logit={err_logit:.2e} err_reg={np.array2string(err_reg, precision=2)}")
 
