@@ -148,11 +148,66 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
-__device__ __forceinline__ float tanh_approx(float x) {
+__device__ __forceinline__ float tanh_approx(float x) {   // MUFU.TANH, |error| <= 7.9e-6 (measured)
     float y;
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// tanh(x) = 1 - 2 / (1 + 2^(2x log2 e)) with MUFU ex2 + rcp (~2^-22 relative each): |error|
+// <~ 5e-7.  Used where a trained network amplifies activation error the most (the
+// classifier's first hidden layer); saturates cleanly
+// (e = inf -> 1, e = 0 -> -1).
+__device__ __forceinline__ float tanh_accurate(float x) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 2.8853900817779268f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+    return fmaf(-2.f, r, 1.f);
+}
+// Odd/even rational tanh(x) = x P(x^2) / Q(x^2) on [-9, 9] (|error| <~ 4e-7 in fp32; the
+// paper's own inference also uses a rational tanh): one MUFU rcp per value, the
+// polynomials in packed FFMA2 (two activations per instruction).
+__device__ __forceinline__ float2 tanh_rational2(float2 x) {
+    x.x = fminf(fmaxf(x.x, -9.f), 9.f);
+    x.y = fminf(fmaxf(x.y, -9.f), 9.f);
+    const float2 x2 = __fmul2_rn(x, x);
+    auto c = [](float v) { return make_float2(v, v); };
+    float2 p = __ffma2_rn(x2, c(-2.76076847742355e-16f), c(2.00018790482477e-13f));
+    p = __ffma2_rn(x2, p, c(-8.60467152213735e-11f));
+    p = __ffma2_rn(x2, p, c(5.12229709037114e-08f));
+    p = __ffma2_rn(x2, p, c(1.48572235717979e-05f));
+    p = __ffma2_rn(x2, p, c(6.37261928875436e-04f));
+    p = __ffma2_rn(x2, p, c(4.89352455891786e-03f));
+    p = __fmul2_rn(p, x);
+    float2 q = __ffma2_rn(x2, c(1.19825839466702e-06f), c(1.18534705686654e-04f));
+    q = __ffma2_rn(x2, q, c(2.26843463243900e-03f));
+    q = __ffma2_rn(x2, q, c(4.89352518554385e-03f));
+    float2 r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(q.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(q.y));
+    return __fmul2_rn(p, r);
+}
+// tanh via one MUFU ex2 and a reciprocal by Newton iterations on the FMA pipe (packed):
+// d = 1 + e in [1, 2^26] (x clamped to 9), r0 from the exponent bit trick (~1/8 relative),
+// three Newton steps (error 2^-3 -> 2^-6 -> 2^-12 -> 2^-24).
+__device__ __forceinline__ float2 tanh_ex2_newton2(float2 x) {
+    x.x = fminf(x.x, 9.f);
+    x.y = fminf(x.y, 9.f);
+    const float2 a = __fmul2_rn(x, make_float2(2.8853900817779268f, 2.8853900817779268f));
+    float2 e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a.y));
+    const float2 one = make_float2(1.f, 1.f), two = make_float2(2.f, 2.f);
+    const float2 d = __fadd2_rn(e, one);
+    float2 r = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(d.x)),
+                           __int_as_float(0x7EF311C3 - __float_as_int(d.y)));
+    const float2 nd = make_float2(-d.x, -d.y);
+#pragma unroll
+    for (int it = 0; it < 3; ++it) r = __fmul2_rn(r, __ffma2_rn(nd, r, two));
+    return __ffma2_rn(make_float2(-2.f, -2.f), r, one);
+}
+#ifndef PLT_MAP_CLS_TANH
+#define PLT_MAP_CLS_TANH 1   // classifier first hidden layer: 0 MUFU tanh, 1 ex2+rcp, 2 rational
+#endif
 // pack (lo_elem, hi_elem) -> bf16x2 with lo_elem in the low half (lower address)
 __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
     uint32_t d;
@@ -178,39 +233,39 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 
 // A operand in TMEM (kind::f16, M = 128): row m = lane m, element k of the row in 32-bit
 // column k/2 (even k in the low half).  Hidden/output layers read K = 80: columns 0-15
-// hold bf16(h) (hi), 16-31 the bf16 residual h - hi (lo), 32-39 the constant (1, 1, 0..)
-// chunk that multiplies the folded bias hi/lo column pair of B.
-// bf16 pair packing by truncation: hi = top 16 bits of each float (exactly a bf16), one PRMT
-// per pair; the residual lo = x - hi is exact in fp32 and rounded once to bf16, so
-// hi + lo carries ~16 mantissa bits exactly as with a rounded hi.
-__device__ __forceinline__ uint32_t pack_hi_trunc(float x0, float x1) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(d) : "r"(__float_as_uint(x0)), "r"(__float_as_uint(x1)));
-    return d;
+// hold bf16(h) (hi, round-to-nearest), 16-31 the bf16 residual h - hi (lo), 32-39 the
+// constant (1, 1, 1, 0, ..) chunk that multiplies the folded bias hi/mid/lo columns of B.
+// hi + lo carries ~17 significant bits of h (the residual is exact in fp32 and rounded
+// once); the 3-term bias is exact for an fp32 bias.
+__device__ __forceinline__ uint32_t split_pair(float x0, float x1, uint32_t& lo) {
+    const uint32_t hi = pack_bf16(x0, x1);
+    lo = pack_bf16(x0 - bf16lo_f(hi), x1 - bf16hi_f(hi));
+    return hi;
 }
-__device__ __forceinline__ float hi_trunc_f(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u); }
 
 // Split 16 activations (D columns c0..c0+15) into hi/lo pairs and store them.
 __device__ __forceinline__ void store_hidden16(uint32_t a_row, int c0, const float (&h)[16]) {
     uint32_t hi[8], lo[8];
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-        const float x0 = h[2 * p], x1 = h[2 * p + 1];
-        hi[p] = pack_hi_trunc(x0, x1);
-        lo[p] = pack_bf16(x0 - hi_trunc_f(x0), x1 - hi_trunc_f(x1));
-    }
+    for (int p = 0; p < 8; ++p) hi[p] = split_pair(h[2 * p], h[2 * p + 1], lo[p]);
     tmem_st8(a_row + c0 / 2, hi);
     tmem_st8(a_row + 16 + c0 / 2, lo);
 }
-// Input-layer A row (K = 16): x_hi[4], x_lo[4], (1, 1) folded-bias pair, zeros.
+// Input-layer A row (K = 16): x_hi[4], x_mid[4], x_lo[4] (an exact 3-term bf16 split of the
+// fp32 inputs), then (1, 1, 1) for the folded bias hi/mid/lo, zero.  The input layer is
+// where trained weights amplify a 2-term split the most.
 __device__ __forceinline__ void store_input(uint32_t a_row, const float (&x)[4]) {
     uint32_t v[8];
-    v[0] = pack_hi_trunc(x[0], x[1]);
-    v[1] = pack_hi_trunc(x[2], x[3]);
-    v[2] = pack_bf16(x[0] - hi_trunc_f(x[0]), x[1] - hi_trunc_f(x[1]));
-    v[3] = pack_bf16(x[2] - hi_trunc_f(x[2]), x[3] - hi_trunc_f(x[3]));
-    v[4] = 0x3F803F80u;   // bf16 (1.0, 1.0)
-    v[5] = 0u; v[6] = 0u; v[7] = 0u;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const float x0 = x[2 * p], x1 = x[2 * p + 1];
+        uint32_t r;
+        v[p] = split_pair(x0, x1, r);
+        const float r0 = x0 - bf16lo_f(v[p]), r1 = x1 - bf16hi_f(v[p]);
+        v[2 + p] = split_pair(r0, r1, v[4 + p]);
+    }
+    v[6] = 0x3F803F80u;   // bf16 (1.0, 1.0)
+    v[7] = 0x00003F80u;   // bf16 (1.0, 0)
     tmem_st8(a_row, v);
 }
 
@@ -326,7 +381,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const uint32_t tmem_a = S.tmem_base + (uint32_t)(32 * G + kACols * g);     // A operand (40 cols)
     const uint32_t a_row = tmem_a + lane_off;
     {   // constant bias-ones chunk (columns 32-39) of this row's A operand
-        const uint32_t ones[8] = {0x3F803F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        const uint32_t ones[8] = {0x3F803F80u, 0x00003F80u, 0u, 0u, 0u, 0u, 0u, 0u};
         tmem_st8(a_row + 32, ones);
         tmem_st_wait();
     }
@@ -395,7 +450,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
 #endif
     };
     // hidden epilogue: TMEM (bias already folded) -> tanh -> hi/lo -> A operand, in two halves
-    auto hidden_epilogue = [&]() {
+    auto hidden_epilogue = [&](bool accurate) {
         PLT_CLK(e0);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
@@ -403,8 +458,25 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             float v[16];
             tmem_ld16(tmem_row + 16 * half, v);
             PLT_CLK(h1);
+            if (accurate && PLT_MAP_CLS_TANH == 1) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
+                for (int j = 0; j < 16; ++j) v[j] = tanh_accurate(v[j]);
+            } else if (accurate && PLT_MAP_CLS_TANH == 3) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const float2 y = tanh_ex2_newton2(make_float2(v[j], v[j + 1]));
+                    v[j] = y.x; v[j + 1] = y.y;
+                }
+            } else if (accurate && PLT_MAP_CLS_TANH == 2) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const float2 y = tanh_rational2(make_float2(v[j], v[j + 1]));
+                    v[j] = y.x; v[j + 1] = y.y;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
+            }
 #ifdef PLT_MAP_PROFILE
             float sink = 0.f;
             for (int j = 0; j < 16; ++j) sink += v[j];
@@ -445,11 +517,11 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         pr_gather += clock64() - g0;
 #endif
         mma_layer(true, P.lay.reg_w[0], 32);
-        hidden_epilogue();
+        hidden_epilogue(false);
 #pragma unroll 1
         for (int l = 1; l < 4; ++l) {
             mma_layer(false, P.lay.reg_w[l], 32);
-            hidden_epilogue();
+            hidden_epilogue(false);
         }
         mma_layer(false, P.lay.reg_w[4], 32);
         float y[6];
@@ -498,7 +570,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         tmem_st_wait();
         PLT_CLK(o1);
         mma_layer(true, P.lay.cls_w[0], 32);
-        hidden_epilogue();
+        hidden_epilogue(true);
         mma_layer(false, P.lay.cls_w[1], 32);
         PLT_CLK(o2);
         float lg[1];

@@ -6,8 +6,8 @@
 // shared-memory layout: element (n, k) of a B operand with K columns lives at
 //   (n/8) * (K/8)*128 + (k/8) * 128 + (n%8) * 16 + (k%8) * 2   bytes,
 // i.e. 8-row x 16-byte core matrices, adjacent along K (LBO = 128 B) and stacked
-// along N (SBO = K/8 * 128 B).  The input layer's operand duplicates W along K so
-// one K=16 MMA consumes the bf16 hi/lo split of the 4 inputs: k 0..3 = W, 4..7 = W.
+// along N (SBO = K/8 * 128 B).  The input layer's operand repeats W along K so one
+// K=16 MMA consumes the exact bf16 hi/mid/lo split of the 4 inputs: k 0..3, 4..7, 8..11 = W.
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -58,19 +58,23 @@ float bf16_to_f(uint16_t h) {
 }
 
 // Pack W (fo x fi, bf16 bits) and bias b (fo, fp32) into an N = n_pad, K = k_total operand.
-// Input layer (k_total = 16): k 0..fi-1 = W, fi..2fi-1 = W (hi/lo halves of A), 2fi, 2fi+1 =
-// bias hi/lo.  Hidden/output (k_total = 48): k 0..31 = W, 32/33 = bias hi/lo, rest 0.
+// Input layer (k_total = 16): k 0..fi-1, fi..2fi-1, 2fi..3fi-1 = W (against the hi/mid/lo
+// thirds of A), 3fi..3fi+2 = bias hi/mid/lo.  Hidden/output (k_total = 48): k 0..31 = W,
+// 32..34 = bias hi/mid/lo, rest 0.  The 3-term bias split is exact for an fp32 bias.
 void pack_operand(uint8_t* dst, const uint16_t* W, const float* b, int fo, int fi, int n_pad, int k_total,
                   bool input) {
     const int sbo = (k_total / 8) * 128;
-    const int kb = input ? 2 * fi : 32;
+    const int kb = input ? 3 * fi : 32;
     for (int nn = 0; nn < n_pad; ++nn)
         for (int k = 0; k < k_total; ++k) {
             uint16_t v = 0;
             if (nn < fo) {
+                const float bh = bf16_to_f(bf16_rne(b[nn]));
+                const float bm = bf16_to_f(bf16_rne(b[nn] - bh));
                 if (k < kb) { if (input || k < fi) v = W[nn * fi + (k % fi)]; }
                 else if (k == kb) v = bf16_rne(b[nn]);
-                else if (k == kb + 1) v = bf16_rne(b[nn] - bf16_to_f(bf16_rne(b[nn])));
+                else if (k == kb + 1) v = bf16_rne(b[nn] - bh);
+                else if (k == kb + 2) v = bf16_rne(b[nn] - bh - bm);
             }
             const size_t off = (size_t)(nn / 8) * sbo + (k / 8) * 128 + (nn % 8) * 16 + (k % 8) * 2;
             std::memcpy(dst + off, &v, 2);
