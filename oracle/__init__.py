@@ -20,8 +20,9 @@ O/A = SURVEY.md §8(c) steps/readings, restated in DESIGN.md):
 Pins (tests/test_oracle_*.py) tie every function to something other than
 itself: SPEC worked values, closed forms (lensmaker, normal-incidence Fresnel),
 an independent brute-force singlet tracer, symmetry, reciprocity, ABCD
-third-order convergence, torch float64 for the MLP.  The map-vs-trace VALUE
-relation is "parity unpinned" (no trained weights exist).
+third-order convergence, torch float64 for the MLP, and the map-vs-trace relation
+through fitted maps (maps/, trained on this oracle's labels by tests/fit_map.py):
+map_eval reproduces trace to the fitting error (tests/test_oracle_map_vs_trace.py).
 """
 from __future__ import annotations
 
