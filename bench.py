@@ -144,6 +144,18 @@ def dist_setup(args):
     return ws, rank, local
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full capture
+    (profiles/*_ncu_traffic.json); None if there is none.  Never runs ncu itself."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        k = json.load(f)["kernels"].get(kernel)
+    return None if k is None else k["dram_read"] + k["dram_write"]
+
+
 def workload_config(n: int, ws: int, pid: int) -> dict:
     """The `config` object shared by both arms (same workload, metric and unit)."""
     return {"workload": "C2: 50 mm double-Gauss (Kolb/pbrt stand-in), 2^24 rays per GPU, lambda U[400,700] nm, "
@@ -380,7 +392,7 @@ def run_plt(args, ws, rank, local):
     dominant = max(("eval_map", "trace_rays"), key=lambda k: kernels[k]["ms"])
     roof = dict(kernels[dominant]["roofline"])
     roof["kernel"] = dominant
-    roof["traffic"] = None
+    roof["traffic"] = ncu_traffic(dominant)
     value = ws * n / step_s / 1e6
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
