@@ -7,18 +7,18 @@
 // MLP into its render kernels and replaces tanh by an approximation.
 //
 // B200 design:
-//  * one persistent CTA per SM, G = 7 independent "tile pipelines" (groups of 4 warps);
+//  * one persistent CTA per SM, G = 8 independent "tile pipelines" (groups of 4 warps);
 //    a group owns 128 rays = one M=128 tcgen05 tile, thread t of the group = row t =
 //    TMEM lane t (warp q of the group reads TMEM lanes 32q..32q+31);
 //  * every layer is tcgen05.mma.cta_group::1.kind::f16 (bf16 x bf16 -> fp32) with the
-//    activation operand A in TMEM (written by tcgen05.st; 40 columns per group), the
+//    activation operand A in TMEM (written by tcgen05.st; 32 columns per group), the
 //    weights B resident in shared memory (TMA bulk-copied once per CTA) and the
-//    accumulator D in TMEM (32 columns per group) -- 7 x 72 of the 512 TMEM columns;
+//    accumulator D in TMEM (32 columns per group) -- G x 64 of the 512 TMEM columns;
 //  * activations are carried as a bf16 hi/lo pair (A = [h_hi | h_lo], B = W for both
 //    halves), so the contraction keeps ~16 mantissa bits; plain bf16 activations
 //    would exceed the 2e-3 output tolerance (SURVEY [B3]);
-//  * biases are folded into the contraction (a bf16 hi/lo bias column pair in B times a
-//    constant (1, 1) chunk in A); epilogue per layer: tcgen05.ld -> tanh.approx -> split
+//  * biases are folded into the contraction (bf16 hi/mid/lo bias columns in B times a
+//    constant ones A tile shared by all groups in shared memory); epilogue per layer: tcgen05.ld -> tanh.approx -> split
 //    -> tcgen05.st -> named barrier -> one thread issues the next layer's MMAs;
 //  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs;
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
@@ -37,8 +37,10 @@ namespace {
 
 constexpr int kTile = 128;                   // rays per tile (UMMA M)
 constexpr int kQueue = 256;                  // per-group queue capacity (ring of ray indices)
-constexpr int kACols = 40;                   // A operand in TMEM: 80 bf16 per row = 40 columns
-                                             // (cols 0-15 hi, 16-31 lo, 32-39 bias-ones chunk)
+constexpr int kACols = 32;                   // A operand in TMEM: 64 bf16 per row = 32 columns
+                                             // (cols 0-15 hi, 16-31 lo); the bias K-step reads a
+                                             // constant "ones" A tile from shared memory instead
+constexpr int kOnesBytes = kTile * 16 * 2;    // 128 x 16 bf16, canonical K-major (LBO 128, SBO 256)
 constexpr int kNumIn = 5;                    // staged SoA inputs: ox, oy, dx, dy, lambda (dz unused)
 constexpr int kStageBytes = kNumIn * kTile * 4;
 constexpr uint32_t kMaxImageBytes = 20480;
@@ -52,6 +54,7 @@ struct GroupSmem {
 template <int G>
 struct Smem {
     alignas(128) uint8_t w[kMaxImageBytes];   // packed weights (+ folded biases)
+    alignas(128) uint8_t ones[kOnesBytes];    // A operand of every bias K-step: rows (1, 1, 1, 0, ...)
     GroupSmem g[G];
     alignas(8) uint64_t bar_w;                // weights loaded
     alignas(8) uint64_t bar_mma[G];           // MMA complete
@@ -303,18 +306,19 @@ __device__ __forceinline__ Canon canonicalise(const MapParams& mp, float px, flo
 }
 
 // Layer MMAs (A from TMEM, B = weights in shared memory).  Input layer: one K=16 step
-// (x hi/lo + bias-ones).  Hidden / output layers: K = 80 of A (32 hi, 32 lo, 16 bias-ones)
-// against B = [W | bias chunk] stored once as K = 48 (hi and lo reuse the same W columns).
+// (x hi/mid/lo + bias-ones).  Hidden / output layers: K = 64 of A from TMEM (32 hi, 32 lo)
+// plus one K = 16 step whose A is the shared constant ones tile in shared memory, against
+// B = [W | bias chunk] stored once as K = 48 (hi and lo reuse the same W columns).
 __device__ __forceinline__ void issue_input(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base) {
     umma_ts(tmem_d, tmem_a, sdesc(b_base, 128, 256), idesc_bf16(32), 0u);
 }
-__device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base, int n_out) {
+__device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base, uint32_t ones,
+                                             int n_out) {
     const uint32_t id = idesc_bf16(n_out);
 #pragma unroll
-    for (int ks = 0; ks < 5; ++ks) {
-        const int bk = ks < 4 ? (ks & 1) : 2;
-        umma_ts(tmem_d, tmem_a + 8 * ks, sdesc(b_base + bk * 256, 128, 768), id, ks > 0 ? 1u : 0u);
-    }
+    for (int ks = 0; ks < 4; ++ks)   // h hi (ks 0, 1) and lo (ks 2, 3) against W k 0-15 / 16-31
+        umma_ts(tmem_d, tmem_a + 8 * ks, sdesc(b_base + (ks & 1) * 256, 128, 768), id, ks > 0 ? 1u : 0u);
+    umma(tmem_d, sdesc(ones, 128, 256), sdesc(b_base + 2 * 256, 128, 768), id, 1u);   // + bias
 }
 
 // Last hidden layer + fp32 output layer: h = tanh(D) from TMEM, y[o] = b[o] + sum_j W[o][j] h[j]
@@ -378,13 +382,19 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;                        // this warp's lane quarter
     const uint32_t tmem = S.tmem_base + (uint32_t)(32 * g);                    // accumulator (32 cols)
     const uint32_t tmem_row = tmem + lane_off;
-    const uint32_t tmem_a = S.tmem_base + (uint32_t)(32 * G + kACols * g);     // A operand (40 cols)
+    const uint32_t tmem_a = S.tmem_base + (uint32_t)(32 * G + kACols * g);     // A operand (32 cols)
     const uint32_t a_row = tmem_a + lane_off;
-    {   // constant bias-ones chunk (columns 32-39) of this row's A operand
-        const uint32_t ones[8] = {0x3F803F80u, 0x00003F80u, 0u, 0u, 0u, 0u, 0u, 0u};
-        tmem_st8(a_row + 32, ones);
-        tmem_st_wait();
+    // constant bias-ones A tile (shared by all pipelines): element (m, k) at
+    // (m/8)*256 + (k/8)*128 + (m%8)*16 + (k%8)*2; k = 0, 1, 2 -> bf16 1.0 (bias hi/mid/lo)
+    for (int i = tid; i < kOnesBytes / 4; i += blockDim.x) {
+        const int byte = 4 * i, in_core = byte & 127, kchunk = (byte >> 7) & 1, kk = (in_core & 15) >> 1;
+        uint32_t v = 0u;
+        if (kchunk == 0 && kk == 0) v = 0x3F803F80u;        // k = 0, 1
+        else if (kchunk == 0 && kk == 2) v = 0x00003F80u;   // k = 2
+        reinterpret_cast<uint32_t*>(S.ones)[i] = v;
     }
+    fence_proxy_async();   // generic-proxy writes -> visible to the tensor core (async proxy)
+    __syncthreads();
     if (tid == 0) {
         mbar_expect_tx(&S.bar_w, P.lay.total_bytes);
         tma_bulk_g2s(S.w, P.wimg, P.lay.total_bytes, &S.bar_w);
@@ -406,6 +416,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     };
 
     const uint32_t w_base = smem_u32(S.w);
+    const uint32_t ones_base = smem_u32(S.ones);
     uint32_t mma_phase = 0;
     uint32_t in_phase[2] = {0, 0};
 
@@ -432,7 +443,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             tc_fence_after();
             PLT_CLK(i0);
             if (input) issue_input(tmem, tmem_a, w_base + b_off);
-            else issue_hidden(tmem, tmem_a, w_base + b_off, n_out);
+            else issue_hidden(tmem, tmem_a, w_base + b_off, ones_base, n_out);
             PLT_CLK(i1);
             umma_commit(&S.bar_mma[g]);
 #ifdef PLT_MAP_PROFILE
@@ -672,13 +683,15 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
     P.mp = mp;
     P.wimg = (const uint8_t*)d_weights;
     static const int groups = [] {
-        const char* e = getenv("PLT_MAP_GROUPS");   // tuning knob (4, 6 or 7 tile pipelines per SM)
-        return e ? atoi(e) : 7;
+        const char* e = getenv("PLT_MAP_GROUPS");   // tuning knob (4, 6, 7 or 8 tile pipelines per SM)
+        return e ? atoi(e) : 8;
     }();
     cudaStream_t s = (cudaStream_t)stream;
     if (groups == 4) return launch_groups<4>(P, sms, s);
     if (groups == 6) return launch_groups<6>(P, sms, s);
-    return launch_groups<7>(P, sms, s);
+    if (groups == 8) return launch_groups<8>(P, sms, s);
+    if (groups == 7) return launch_groups<7>(P, sms, s);
+    return launch_groups<8>(P, sms, s);
 }
 
 }  // namespace plt

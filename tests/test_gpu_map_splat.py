@@ -152,6 +152,59 @@ def test_splat_bit_exact_vs_oracle(gpu_lib):
     assert np.allclose(out.cpu().numpy(), ref.reshape(-1) * 2.0 ** -32 * 2.0, rtol=1e-6, atol=0)
 
 
+def _splat_both(plt, f32, valid, ch, scale):
+    import torch
+    n = f32["px"].size
+    ref, dropped = oracle.splat(FILM, valid, f32["px"], f32["py"], f32["dz"], f32["I"], ch, scale=scale)
+    dev = {"px": torch.from_numpy(f32["px"]).cuda(), "py": torch.from_numpy(f32["py"]).cuda(),
+           "dz": torch.from_numpy(f32["dz"]).cuda(), "throughput": torch.from_numpy(f32["I"]).cuda(),
+           "dx": torch.zeros(n, device="cuda"), "dy": torch.zeros(n, device="cuda")}
+    words = np.zeros((n + 31) // 32, np.uint32)
+    for b in range(32):
+        sel = np.arange(b, n, 32)
+        words[sel // 32] |= valid[sel].astype(np.uint32) << np.uint32(b)
+    dev["mask_bits"] = torch.from_numpy(words.view(np.int32)).cuda()
+    film = torch.zeros(3 * FILM["height_px"] * FILM["width_px"], dtype=torch.int64, device="cuda")
+    drop = torch.zeros(1, dtype=torch.int64, device="cuda")
+    plt.splat_sensor(FILM, film, dev, channel=torch.from_numpy(ch).cuda(), weight_scale=scale, dropped=drop)
+    torch.cuda.synchronize()
+    return film.cpu().numpy().reshape(ref.shape), ref, int(drop.item()), dropped
+
+
+@pytest.mark.parametrize("scale", [1.0, 2.0 ** -20, 2.0 ** -7, 2.0 ** 30, 1.0 / 3.0, 0.75],
+                         ids=["1", "2^-20", "2^-7", "2^30", "1/3", "0.75"])
+def test_splat_edges_and_scales_bit_exact(gpu_lib, scale):
+    """Integer-exact weight path (power-of-two scales) and the double path (others) against
+    O11, with hits on pixel edges, film borders, outside the film, and zero / subnormal /
+    tie-producing / negative weights."""
+    plt = gpu_lib
+    rng = np.random.default_rng(12)
+    n = 200_003
+    W, H, wp, hp = FILM["sensor_w_mm"], FILM["sensor_h_mm"], FILM["width_px"], FILM["height_px"]
+    px = rng.uniform(-0.55 * W, 0.55 * W, n)
+    py = rng.uniform(-0.55 * H, 0.55 * H, n)
+    edge = rng.random(n) < 0.3                           # exactly on pixel boundaries / borders
+    px[edge] = (rng.integers(0, wp + 1, edge.sum()) / wp - 0.5) * W
+    py[edge] = (0.5 - rng.integers(0, hp + 1, edge.sum()) / hp) * H
+    I = rng.uniform(0, 1, n)
+    dz = rng.uniform(-1, 1, n)
+    kind = rng.integers(0, 8, n)
+    I[kind == 0] = 0.0
+    I[kind == 1] = 1e-42                                 # subnormal
+    I[kind == 2] = rng.integers(1, 2 ** 10, (kind == 2).sum()) / 2.0 ** 10   # short mantissas: ties
+    dz[kind == 2] = rng.integers(1, 2 ** 10, (kind == 2).sum()) / 2.0 ** 10
+    I[kind == 3] = 1.0
+    dz[kind == 3] = 1.0
+    I[kind == 4] = -I[kind == 4]                         # negative throughput (API allows it)
+    f32 = {"px": px.astype(np.float32), "py": py.astype(np.float32), "dz": dz.astype(np.float32),
+           "I": I.astype(np.float32)}
+    valid = rng.random(n) < 0.9
+    ch = rng.integers(0, 3, n).astype(np.uint8)
+    got, ref, gd, rd = _splat_both(plt, f32, valid, ch, scale)
+    assert gd == rd
+    assert np.array_equal(got, ref), int((got != ref).sum())
+
+
 def test_flare_ghost_end_to_end_fp64(gpu_lib):
     """GPU fp64 trace of one ghost -> GPU splat equals the oracle splat of the GPU hits
     (binding) and the oracle trace->splat film up to bin flips of edge rays."""
