@@ -325,10 +325,21 @@ def run_plt(args, ws, rank, local):
     # ---------------- e2e: host buffers -> device -> step -> film back to host ----------
     e2e_steps = max(3, min(args.steps, 10))
 
+    from paper_2605_04017_b200.pipeline import query_host_batch
+    host_rays = dict(host, plane_z=rays_np["plane_z"])
+    copy_stream = torch.cuda.Stream(device=dev)
+    chunk = 1 << 21
+    copy_done = [torch.cuda.Event() for _ in range((n + chunk - 1) // chunk)]
+
     def e2e_step():
-        for k in plt.RAY_KEYS:
-            d_rays[k].copy_(host[k], non_blocking=True)
-        step()
+        # the public host-batch path: chunked H2D on a copy stream overlapping the kernels
+        lens.enumerate_ghosts(0)
+        film.zero_()
+        query_host_batch(lens, pid, m, host_rays, d_rays, h_trace, h_map, FILM, film, None,
+                         weight_scale=1.0 / n, chunk=chunk, compute_stream=stream, copy_stream=copy_stream,
+                         copy_done=copy_done)
+        if dist is not None:
+            dist.all_reduce(film)
         film_host.copy_(film, non_blocking=True)
 
     e2e_step()

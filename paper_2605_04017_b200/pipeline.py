@@ -1,0 +1,63 @@
+"""Host-resident ray batches: chunked copy/compute overlap on two CUDA streams.
+
+The per-ray query (trace + map + splat) is ~0.11 ns per ray on a B200,
+while moving its 24 B of inputs over PCIe costs ~0.45 ns: a batch that lives in host
+memory is bound by the host->device copy.  `query_host_batch` splits the batch into
+chunks, copies chunk c+1 on a copy stream while the kernels of chunk c run on the
+compute stream (event-ordered, no host synchronisation), and returns the film to pinned
+host memory at the end.  Orchestration only: every step runs in the library's kernels
+through the C-ABI calls of this package.
+"""
+from __future__ import annotations
+
+from . import RAY_KEYS, eval_map, splat_sensor, trace_rays
+
+
+def _view(d: dict, lo: int, hi: int) -> dict:
+    out = {k: v[lo:hi] for k, v in d.items() if k not in ("plane_z", "mask_bits", "flags")}
+    if "plane_z" in d:
+        out["plane_z"] = d["plane_z"]
+    if "mask_bits" in d:
+        out["mask_bits"] = d["mask_bits"][lo // 32:(hi + 31) // 32]
+    if d.get("flags") is not None:
+        out["flags"] = d["flags"][lo:hi]
+    return out
+
+
+def query_host_batch(lens, path_id: int, m, host_rays: dict, d_rays: dict, h_trace: dict, h_map: dict,
+                     film_desc: dict, film, film_host=None, weight_scale: float = 1.0, chunk: int = 1 << 21,
+                     compute_stream=None, copy_stream=None, copy_done=None):
+    """Trace + map + splat a batch whose inputs are in (pinned) host memory.
+
+    host_rays: pinned CPU float32 tensors (RAY_KEYS) + "plane_z"; d_rays / h_trace / h_map:
+    device buffers of at least the batch size; film: device int64 film (accumulated, not
+    cleared); film_host: optional pinned int64 tensor that receives the film.  chunk must
+    be a multiple of 32 (mask words).  All work is enqueued; nothing synchronises the host.
+    """
+    import torch
+    if chunk % 32:
+        raise ValueError("chunk must be a multiple of 32")
+    n = int(host_rays["ox"].numel())
+    cs = compute_stream or torch.cuda.current_stream()
+    xs = copy_stream or torch.cuda.Stream(device=film.device)
+    if copy_done is None:
+        copy_done = [torch.cuda.Event() for _ in range((n + chunk - 1) // chunk)]
+    xs.wait_stream(cs)                      # buffers are free once earlier work on cs is done
+    for c, lo in enumerate(range(0, n, chunk)):
+        hi = min(n, lo + chunk)
+        with torch.cuda.stream(xs):
+            for k in RAY_KEYS:
+                d_rays[k][lo:hi].copy_(host_rays[k][lo:hi], non_blocking=True)
+            copy_done[c].record(xs)
+        cs.wait_event(copy_done[c])
+        dv = _view(d_rays, lo, hi)
+        dv["plane_z"] = host_rays["plane_z"]
+        ht, hm = _view(h_trace, lo, hi), _view(h_map, lo, hi)
+        trace_rays(lens, path_id, dv, ht, stream=cs)
+        eval_map(m, dv, hm, stream=cs)
+        splat_sensor(film_desc, film, ht, weight_scale=weight_scale, stream=cs)
+        splat_sensor(film_desc, film, hm, weight_scale=weight_scale, stream=cs)
+    if film_host is not None:
+        with torch.cuda.stream(cs):
+            film_host.copy_(film, non_blocking=True)
+    return film_host
