@@ -242,7 +242,8 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // once); the 3-term bias is exact for an fp32 bias.
 __device__ __forceinline__ uint32_t split_pair(float x0, float x1, uint32_t& lo) {
     const uint32_t hi = pack_bf16(x0, x1);
-    lo = pack_bf16(x0 - bf16lo_f(hi), x1 - bf16hi_f(hi));
+    const float2 r = __fadd2_rn(make_float2(x0, x1), make_float2(-bf16lo_f(hi), -bf16hi_f(hi)));   // exact
+    lo = pack_bf16(r.x, r.y);
     return hi;
 }
 
@@ -289,9 +290,14 @@ struct Params {
 struct Canon { float x[4]; float c, s; bool flip; };
 __device__ __forceinline__ Canon canonicalise(const MapParams& mp, float px, float py, float wx, float wy, float lam) {
     Canon k;
-    const float r = sqrtf(px * px + py * py);
-    if (r > 0.f) { const float ir = 1.f / r; k.c = px * ir; k.s = py * ir; }
-    else {
+    const float r2 = fmaf(px, px, py * py);
+    float r = 0.f;
+    if (r2 > 0.f) {   // MUFU rsqrt + one Newton step (~1 ulp; the oracle's tolerance is 2e-3)
+        float ir;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ir) : "f"(r2));
+        ir = ir * fmaf(-0.5f * r2 * ir, ir, 1.5f);
+        r = r2 * ir; k.c = px * ir; k.s = py * ir;
+    } else {
         const float tt = sqrtf(wx * wx + wy * wy);
         if (tt > 0.f) { k.c = wx / tt; k.s = wy / tt; } else { k.c = 1.f; k.s = 0.f; }
     }
@@ -322,11 +328,32 @@ __device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t tmem_a, u
 }
 
 // Last hidden layer + fp32 output layer: h = tanh(D) from TMEM, y[o] = b[o] + sum_j W[o][j] h[j]
-// (weights broadcast from shared memory) -- no MMA round for the 1- or 6-wide output.
-template <int NOUT>
-__device__ __forceinline__ void output_epilogue(uint32_t tmem_row, const float* W, const float* b, float (&y)[NOUT]) {
+// (weights broadcast from shared memory) -- no MMA round for the 1- or 6-wide output.  The
+// dot products issue as packed FFMA2: the classifier's single output accumulates even/odd
+// j in the two halves; the regressor's outputs go in pairs (2p, 2p+1) against the block's
+// pair-interleaved weights Wp[p][j] = (W[2p][j], W[2p+1][j]) (map.cpp).
+__device__ __forceinline__ void output_epilogue_cls(uint32_t tmem_row, const float* W, const float* b, float& y) {
+    float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int o = 0; o < NOUT; ++o) y[o] = b[o];
+    for (int half = 0; half < 2; ++half) {
+        float v[16];
+        tmem_ld16(tmem_row + 16 * half, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
+        const float4* w4 = reinterpret_cast<const float4*>(W + 16 * half);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 w = w4[q4];
+            acc = __ffma2_rn(make_float2(w.x, w.y), make_float2(v[4 * q4], v[4 * q4 + 1]), acc);
+            acc = __ffma2_rn(make_float2(w.z, w.w), make_float2(v[4 * q4 + 2], v[4 * q4 + 3]), acc);
+        }
+    }
+    y = b[0] + (acc.x + acc.y);
+}
+__device__ __forceinline__ void output_epilogue_reg(uint32_t tmem_row, const float* Wp, const float* b, float (&y)[6]) {
+    float2 acc[3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) acc[p] = make_float2(b[2 * p], b[2 * p + 1]);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         float v[16];
@@ -334,18 +361,18 @@ __device__ __forceinline__ void output_epilogue(uint32_t tmem_row, const float* 
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
 #pragma unroll
-        for (int o = 0; o < NOUT; ++o) {
-            const float4* w4 = reinterpret_cast<const float4*>(W + o * 32 + 16 * half);
-            float acc = y[o];
+        for (int p = 0; p < 3; ++p) {
+            const float4* w4 = reinterpret_cast<const float4*>(Wp + 2 * (32 * p + 16 * half));
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                const float4 w = w4[q4];
-                acc = fmaf(w.x, v[4 * q4], acc); acc = fmaf(w.y, v[4 * q4 + 1], acc);
-                acc = fmaf(w.z, v[4 * q4 + 2], acc); acc = fmaf(w.w, v[4 * q4 + 3], acc);
+            for (int q = 0; q < 8; ++q) {
+                const float4 w = w4[q];   // (W[2p][j], W[2p+1][j], W[2p][j+1], W[2p+1][j+1]), j = 2q
+                acc[p] = __ffma2_rn(make_float2(w.x, w.y), make_float2(v[2 * q], v[2 * q]), acc[p]);
+                acc[p] = __ffma2_rn(make_float2(w.z, w.w), make_float2(v[2 * q + 1], v[2 * q + 1]), acc[p]);
             }
-            y[o] = acc;
         }
     }
+#pragma unroll
+    for (int p = 0; p < 3; ++p) { y[2 * p] = acc[p].x; y[2 * p + 1] = acc[p].y; }
 }
 
 template <int G>
@@ -536,7 +563,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         }
         mma_layer(false, P.lay.reg_w[4], 32);
         float y[6];
-        output_epilogue<6>(tmem_row, outw + kOutRegW, outw + kOutRegB, y);
+        output_epilogue_reg(tmem_row, outw + kOutRegW, outw + kOutRegB, y);
         if (live) {
             float o[6];
 #pragma unroll
@@ -584,9 +611,8 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         hidden_epilogue(true);
         mma_layer(false, P.lay.cls_w[1], 32);
         PLT_CLK(o2);
-        float lg[1];
-        output_epilogue<1>(tmem_row, outw + kOutClsW, outw + kOutClsB, lg);
-        const float logit = lg[0];
+        float logit;
+        output_epilogue_cls(tmem_row, outw + kOutClsW, outw + kOutClsB, logit);
         PLT_CLK(o3);
         const bool valid = in_range && logit >= 0.f;     // g(x) = 1 <=> logit >= 0 (A13)
         // ---- mask word + zeros for blocked rays -----------------------------------------

@@ -136,8 +136,12 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
             if (l + 1 == nl) {   // output layer: fp32 block
                 float* wo = outw + (head == 0 ? kOutClsW : kOutRegW);
                 float* bo = outw + (head == 0 ? kOutClsB : kOutRegB);
+                // classifier: W[0][k] as is; regressor: pair-interleaved Wp[p][k] = (W[2p][k], W[2p+1][k])
                 for (uint32_t o = 0; o < fo; ++o) {
-                    for (uint32_t k = 0; k < fi; ++k) wo[o * fi + k] = bf16_to_f(W[o * fi + k]);
+                    for (uint32_t k = 0; k < fi; ++k) {
+                        const size_t at = head == 0 ? o * fi + k : ((o / 2) * fi + k) * 2 + (o & 1);
+                        wo[at] = bf16_to_f(W[o * fi + k]);
+                    }
                     bo[o] = b[o];
                 }
                 continue;
