@@ -9,7 +9,9 @@ lambda uniform 400-700 nm, synthetic seeded rays):
   a8  enumerate_ghosts (host; lists the lens's transport paths)
   a6-a7 trace_rays  -- exact sequential all-T trace (fp32 + fp64 guard-band refine)
   a1-a5 eval_map    -- fused classifier-gated regressor (tcgen05/TMEM)
-  a9  splat_sensor  -- both results splatted into an int64 film (768x512, 36x24 mm)
+  a9  splat_sensor  -- both results splatted into an int64 film (768x512, 36x24 mm); by
+        default fused into the trace / regressor epilogues (plt_*_splat, bit-identical
+        film); --splat separate runs plt_splat_sensor on the hits instead
   a10 film all-reduce over NCCL (N > 1)
 Every ray is queried both ways, so value = rays per step (all ranks) / step time.
 Scaling is weak: each rank owns its own chunk-aligned slice of the global index range.
@@ -249,6 +251,7 @@ def run_plt(args, ws, rank, local):
     from plt_inputs import configs as C
 
     plt.load()
+    fused = args.splat == "fused"
     dev = torch.device("cuda", local)
     n = args.rays
     cfg, rays_np = make_workload(rank, n)
@@ -278,14 +281,16 @@ def run_plt(args, ws, rank, local):
         film.zero_()
         if ev:
             ev[0].record(stream)
-        plt.trace_rays(lens, pid, d_rays, h_trace, stream=stream)          # a6-a7
+        spl = {"film_desc": FILM, "film": film, "weight_scale": 1.0 / n} if fused else None
+        plt.trace_rays(lens, pid, d_rays, h_trace, stream=stream, splat=spl)          # a6-a7 (+a9 fused)
         if ev:
             ev[1].record(stream)
-        plt.eval_map(m, d_rays, h_map, stream=stream)                      # a1-a5
+        plt.eval_map(m, d_rays, h_map, stream=stream, splat=spl)                      # a1-a5 (+a9 fused)
         if ev:
             ev[2].record(stream)
-        plt.splat_sensor(FILM, film, h_trace, weight_scale=1.0 / n, stream=stream)   # a9
-        plt.splat_sensor(FILM, film, h_map, weight_scale=1.0 / n, stream=stream)
+        if not fused:
+            plt.splat_sensor(FILM, film, h_trace, weight_scale=1.0 / n, stream=stream)   # a9
+            plt.splat_sensor(FILM, film, h_map, weight_scale=1.0 / n, stream=stream)
         if ev:
             ev[3].record(stream)
         if dist is not None:
@@ -337,7 +342,7 @@ def run_plt(args, ws, rank, local):
         film.zero_()
         query_host_batch(lens, pid, m, host_rays, d_rays, h_trace, h_map, FILM, film, None,
                          weight_scale=1.0 / n, chunk=chunk, compute_stream=stream, copy_stream=copy_stream,
-                         copy_done=copy_done)
+                         copy_done=copy_done, fused=fused)
         if dist is not None:
             dist.all_reduce(film)
         film_host.copy_(film, non_blocking=True)
@@ -397,7 +402,8 @@ def run_plt(args, ws, rank, local):
                                     "flops_per_ray": trace_flops_per_ray_c2()},
                        "hbm_GBs": trace_bytes / per_step["trace_rays"] / 1e9,
                        "hbm_frac": trace_bytes / per_step["trace_rays"] / 1e9 / float(peaks["hbm_gbs"])},
-        "splat_sensor": {"ms": per_step["splat_sensor"] * 1e3},
+        "splat_sensor": {"ms": per_step["splat_sensor"] * 1e3,
+                         "mode": "fused into trace_rays / eval_map epilogues" if fused else "separate kernel"},
         "film_allreduce": {"ms": per_step["film_allreduce"] * 1e3},
     }
     dominant = max(("eval_map", "trace_rays"), key=lambda k: kernels[k]["ms"])
@@ -414,7 +420,7 @@ def run_plt(args, ws, rank, local):
         "kernels": kernels,
         "e2e": {"value": ws * n / e2e_s / 1e6, "unit": UNIT,
                 "h2d_bytes_per_step": 6 * 4 * n, "d2h_bytes_per_step": npx * 8},
-        "gpu_launches": args.steps * 5,
+        "gpu_launches": args.steps * (3 if fused else 5),
         "clocks": clocks,
         "peaks_source": peaks_src,
     }
@@ -432,6 +438,8 @@ def main():
     ap.add_argument("--rays", type=int, default=1 << 24, help="rays per GPU per step")
     ap.add_argument("--ref-rays", type=int, default=1 << 15, help="rays per oracle step (--impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--splat", choices=["fused", "separate"], default="fused",
+                    help="splat in the query kernels' epilogues (default) or as a separate kernel")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
     try:

@@ -222,6 +222,30 @@ PLT_API plt_status plt_splat_sensor(const plt_film_desc* film_desc, int64_t* fil
                             const uint8_t* channel, float weight_scale, int64_t n,
                             unsigned long long* dropped, void* cuda_stream);
 
+/*
+ * Fused query + splat.  plt_trace_rays_splat / plt_eval_map_splat compute exactly what
+ * plt_trace_rays / plt_eval_map compute (same hits written to `out`) AND splat every valid
+ * hit into splat->film inside the same kernels (the epilogue of the trace / of the
+ * regressor), with the arithmetic of plt_splat_sensor: the film is bit-identical to
+ * calling the query and then plt_splat_sensor on its hits, without re-reading the hits
+ * or a separate launch.  splat->channel (nullable, device, n bytes) is indexed like the
+ * rays.  For PLT_FP32 traces, rays inside a guard band are splatted after their float64
+ * re-trace.  Errors: as the query, plus PLT_E_INVALID_ARG for a bad film description.
+ */
+typedef struct {
+    const plt_film_desc* film_desc;
+    int64_t* film;                  /* device, caller-owned, NOT cleared */
+    const uint8_t* channel;         /* nullable, device, n bytes */
+    float weight_scale;
+    unsigned long long* dropped;    /* nullable device counter */
+} plt_splat_target;
+
+PLT_API plt_status plt_trace_rays_splat(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                                        const plt_rays* in, const plt_hits* out, const plt_splat_target* splat,
+                                        int64_t n, void* cuda_stream);
+PLT_API plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out,
+                                      const plt_splat_target* splat, int64_t n, void* cuda_stream);
+
 /* out[i] = film[i] * 2^-32 * scale (float), for channels*height*width pixels. */
 PLT_API plt_status plt_film_resolve(const plt_film_desc* film_desc, const int64_t* film, float* out,
                             double scale, void* cuda_stream);

@@ -28,7 +28,7 @@ _STATUS = {0: "PLT_OK", 1: "PLT_E_INVALID_ARG", 2: "PLT_E_PARSE", 3: "PLT_E_VALI
 
 EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "plt_lens_info",
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
-            "plt_splat_sensor", "plt_film_resolve")
+            "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat")
 
 
 class PltError(RuntimeError):
@@ -59,6 +59,11 @@ class FilmDesc(C.Structure):
                 ("center_x_mm", C.c_double), ("center_y_mm", C.c_double)]
 
 
+class SplatTarget(C.Structure):
+    _fields_ = [("film_desc", C.c_void_p), ("film", C.c_void_p), ("channel", C.c_void_p),
+                ("weight_scale", C.c_float), ("dropped", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -86,8 +91,11 @@ def load():
     L.plt_eval_map.argtypes = [p, p, p, p, i64, p]
     L.plt_splat_sensor.argtypes = [p, p, p, p, C.c_float, i64, p, p]
     L.plt_film_resolve.argtypes = [p, p, p, d, p]
+    L.plt_trace_rays_splat.argtypes = [p, u64, i, i, p, p, p, i64, p]
+    L.plt_eval_map_splat.argtypes = [p, p, p, p, p, i64, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
-              "plt_eval_map", "plt_splat_sensor", "plt_film_resolve"):
+              "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
+              "plt_eval_map_splat"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -236,22 +244,46 @@ def _n_of(rays, n):
     return int(rays["ox"].numel()) if n is None else int(n)
 
 
+def _splat_struct(splat: dict, n: int):
+    """splat = {"film_desc": dict, "film": int64 tensor, "channel": uint8 tensor | None,
+    "weight_scale": float, "dropped": int64 tensor | None} -> (SplatTarget, keep-alive)."""
+    import torch
+    fd = film_desc(splat["film_desc"])
+    npx = fd.channels * fd.height_px * fd.width_px
+    ch, dr = splat.get("channel"), splat.get("dropped")
+    t = SplatTarget(C.addressof(fd), _ptr(splat["film"], npx, torch.int64),
+                    _ptr(ch, n, torch.uint8) if ch is not None else None, float(splat.get("weight_scale", 1.0)),
+                    _ptr(dr, 1, torch.int64) if dr is not None else None)
+    return t, fd
+
+
 def trace_rays(lens: Lens, path_id: int, rays: dict, hits: dict, direction: int = FORWARD,
-               precision: int = FP32, n: int | None = None, stream=None):
-    """plt_trace_rays (exact sequential trace of one path, Eq. 5-7)."""
+               precision: int = FP32, n: int | None = None, stream=None, splat: dict | None = None):
+    """plt_trace_rays (exact sequential trace of one path, Eq. 5-7); with `splat`,
+    plt_trace_rays_splat (the valid hits are also splatted into splat["film"] in-kernel)."""
     n = _n_of(rays, n)
     r, h = _rays_struct(rays, n), _hits_struct(hits, n)
-    _check(load().plt_trace_rays(lens.handle, int(path_id), direction, precision, C.byref(r), C.byref(h), n,
-                                 _stream(stream)))
+    if splat is None:
+        _check(load().plt_trace_rays(lens.handle, int(path_id), direction, precision, C.byref(r), C.byref(h), n,
+                                     _stream(stream)))
+    else:
+        t, _keep = _splat_struct(splat, n)
+        _check(load().plt_trace_rays_splat(lens.handle, int(path_id), direction, precision, C.byref(r), C.byref(h),
+                                           C.byref(t), n, _stream(stream)))
 
 
-def eval_map(m: Map, rays: dict, hits: dict, raw=None, n: int | None = None, stream=None):
-    """plt_eval_map (fused classifier-gated regressor on tcgen05)."""
+def eval_map(m: Map, rays: dict, hits: dict, raw=None, n: int | None = None, stream=None, splat: dict | None = None):
+    """plt_eval_map (fused classifier-gated regressor on tcgen05); with `splat`,
+    plt_eval_map_splat (valid outputs also splatted in the regressor epilogue)."""
     import torch
     n = _n_of(rays, n)
     r, h = _rays_struct(rays, n), _hits_struct(hits, n)
     rp = _ptr(raw, 7 * n, torch.float32) if raw is not None else None
-    _check(load().plt_eval_map(m.handle, C.byref(r), C.byref(h), rp, n, _stream(stream)))
+    if splat is None:
+        _check(load().plt_eval_map(m.handle, C.byref(r), C.byref(h), rp, n, _stream(stream)))
+    else:
+        t, _keep = _splat_struct(splat, n)
+        _check(load().plt_eval_map_splat(m.handle, C.byref(r), C.byref(h), rp, C.byref(t), n, _stream(stream)))
 
 
 def film_desc(d: dict) -> FilmDesc:

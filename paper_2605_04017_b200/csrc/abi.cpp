@@ -111,8 +111,40 @@ plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, double mi
     PLT_GUARD_END
 }
 
+static bool film_desc_ok(const plt_film_desc* fd) {
+    return fd && fd->width_px > 0 && fd->height_px > 0 && fd->channels > 0 && fd->sensor_w_mm > 0 &&
+           fd->sensor_h_mm > 0 && std::isfinite(fd->center_x_mm) && std::isfinite(fd->center_y_mm);
+}
+
+// Validate a fused-splat target; on success *sc holds the kernel constants.
+static plt_status splat_target(const plt_splat_target* t, plt::SplatCtx* sc) {
+    *sc = plt::SplatCtx{};
+    sc->film = nullptr;
+    if (!t) return PLT_OK;
+    if (!t->film || !film_desc_ok(t->film_desc)) return set_err(PLT_E_INVALID_ARG, "bad splat target (film / film_desc)");
+    *sc = plt::make_splat_ctx(*t->film_desc, t->film, t->channel, t->weight_scale, t->dropped);
+    return PLT_OK;
+}
+
+static plt_status trace_impl(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                             const plt_rays* in, const plt_hits* out, const plt_splat_target* splat, int64_t n,
+                             void* cuda_stream);
+
 plt_status plt_trace_rays(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
                           const plt_rays* in, const plt_hits* out, int64_t n, void* cuda_stream) {
+    return trace_impl(lens, path_id, dir, prec, in, out, nullptr, n, cuda_stream);
+}
+
+plt_status plt_trace_rays_splat(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                                const plt_rays* in, const plt_hits* out, const plt_splat_target* splat, int64_t n,
+                                void* cuda_stream) {
+    if (!splat) return set_err(PLT_E_INVALID_ARG, "splat target is null");
+    return trace_impl(lens, path_id, dir, prec, in, out, splat, n, cuda_stream);
+}
+
+static plt_status trace_impl(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                             const plt_rays* in, const plt_hits* out, const plt_splat_target* splat, int64_t n,
+                             void* cuda_stream) {
     PLT_GUARD_BEGIN
     if (!lens) return set_err(PLT_E_INVALID_ARG, "lens is null");
     if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
@@ -122,10 +154,14 @@ plt_status plt_trace_rays(const plt_lens* lens, uint64_t path_id, plt_dir dir, p
     if (n == 0) return PLT_OK;
     if (!rays_ok(in) || !hits_ok(out)) return set_err(PLT_E_INVALID_ARG, "null ray/hit pointer or non-finite plane z");
     if (n >= (int64_t)1 << 31) return set_err(PLT_E_INVALID_ARG, "n must be < 2^31 per call");
-    plt_status s = check_device();
+    plt::SplatCtx sc;
+    plt_status s = splat_target(splat, &sc);
     if (s != PLT_OK) return s;
-    if (prec == PLT_FP32) return cuda_status(plt::launch_trace_fp32(cp->pf, cp->pd, *in, *out, n, cuda_stream), "trace_rays");
-    return cuda_status(plt::launch_trace_fp64(cp->pd, *in, *out, n, cuda_stream), "trace_rays(fp64)");
+    s = check_device();
+    if (s != PLT_OK) return s;
+    if (prec == PLT_FP32)
+        return cuda_status(plt::launch_trace_fp32(cp->pf, cp->pd, *in, *out, n, cuda_stream, sc), "trace_rays");
+    return cuda_status(plt::launch_trace_fp64(cp->pd, *in, *out, n, cuda_stream, sc), "trace_rays(fp64)");
     PLT_GUARD_END
 }
 
@@ -139,15 +175,32 @@ plt_status plt_map_load(const plt_lens* lens, const void* blob, size_t len, plt_
 
 void plt_map_free(plt_map* map) { delete map; }
 
+static plt_status eval_map_impl(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out,
+                                const plt_splat_target* splat, int64_t n, void* cuda_stream);
+
 plt_status plt_eval_map(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out, int64_t n,
                         void* cuda_stream) {
+    return eval_map_impl(map, in, out, raw_out, nullptr, n, cuda_stream);
+}
+
+plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out,
+                              const plt_splat_target* splat, int64_t n, void* cuda_stream) {
+    if (!splat) return set_err(PLT_E_INVALID_ARG, "splat target is null");
+    return eval_map_impl(map, in, out, raw_out, splat, n, cuda_stream);
+}
+
+static plt_status eval_map_impl(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out,
+                                const plt_splat_target* splat, int64_t n, void* cuda_stream) {
     PLT_GUARD_BEGIN
     if (!map) return set_err(PLT_E_INVALID_ARG, "map is null");
     if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
     if (n == 0) return PLT_OK;
     if (!rays_ok(in) || !hits_ok(out)) return set_err(PLT_E_INVALID_ARG, "null ray/hit pointer");
     if (n >= (int64_t)1 << 31) return set_err(PLT_E_INVALID_ARG, "n must be < 2^31 per call");
-    plt_status s = check_device();
+    plt::SplatCtx sc;
+    plt_status s = splat_target(splat, &sc);
+    if (s != PLT_OK) return s;
+    s = check_device();
     if (s != PLT_OK) return s;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -165,7 +218,7 @@ plt_status plt_eval_map(const plt_map* map, const plt_rays* in, const plt_hits* 
             d_img = it->second;
         }
     }
-    return cuda_status(plt::launch_eval_map(d_img, map->layout, map->params, *in, *out, raw_out, n, cuda_stream),
+    return cuda_status(plt::launch_eval_map(d_img, map->layout, map->params, *in, *out, raw_out, n, cuda_stream, sc),
                        "eval_map");
     PLT_GUARD_END
 }
@@ -174,8 +227,7 @@ plt_status plt_splat_sensor(const plt_film_desc* fd, int64_t* film, const plt_hi
                             float weight_scale, int64_t n, unsigned long long* dropped, void* cuda_stream) {
     PLT_GUARD_BEGIN
     if (!fd || !film || !hits) return set_err(PLT_E_INVALID_ARG, "null film/hits");
-    if (fd->width_px <= 0 || fd->height_px <= 0 || fd->channels <= 0 || !(fd->sensor_w_mm > 0) || !(fd->sensor_h_mm > 0))
-        return set_err(PLT_E_INVALID_ARG, "bad film description");
+    if (!film_desc_ok(fd)) return set_err(PLT_E_INVALID_ARG, "bad film description");
     if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
     if (n == 0) return PLT_OK;
     if (!hits->mask_bits || !hits->px || !hits->py || !hits->dz || !hits->throughput)

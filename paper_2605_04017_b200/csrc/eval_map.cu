@@ -30,6 +30,7 @@
 #include <cstdio>
 
 #include "plt_internal.h"
+#include "splat_dev.cuh"
 
 namespace plt {
 
@@ -49,6 +50,7 @@ struct GroupSmem {
     alignas(16) float stage[2][kNumIn][kTile];  // TMA-staged ray inputs
     int qi[kQueue];                          // queued valid ray indices
     int wcount[4];                           // per-warp valid counts (prefix)
+    long long wsum[kTile];                   // fused splat: per-warp aggregation slots
 };
 
 template <int G>
@@ -283,6 +285,7 @@ struct Params {
     MapLayout lay;
     MapParams mp;
     const uint8_t* wimg;   // device weight image
+    SplatCtx sc;           // fused splat of the valid outputs (sc.film == nullptr: none)
 };
 
 // Canonicalisation of §4.1 (Eq. 10): rotate p onto +x, reflect so w'_y >= 0,
@@ -564,21 +567,26 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         mma_layer(false, P.lay.reg_w[4], 32);
         float y[6];
         output_epilogue_reg(tmem_row, outw + kOutRegW, outw + kOutRegB, y);
-        if (live) {
-            float o[6];
+        float o[6];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) o[d] = P.mp.out_mid[d] + P.mp.out_half[d] * y[d];
-            if (k.flip) { o[1] = -o[1]; o[3] = -o[3]; }  // undo the reflection
-            const float ox = k.c * o[0] - k.s * o[1], oy = k.s * o[0] + k.c * o[1];
-            const float wx2 = k.c * o[2] - k.s * o[3], wy2 = k.s * o[2] + k.c * o[3], wz2 = o[4];
-            const float inv = rsqrtf(wx2 * wx2 + wy2 * wy2 + wz2 * wz2);
+        for (int d = 0; d < 6; ++d) o[d] = P.mp.out_mid[d] + P.mp.out_half[d] * y[d];
+        if (k.flip) { o[1] = -o[1]; o[3] = -o[3]; }  // undo the reflection
+        const float ox = k.c * o[0] - k.s * o[1], oy = k.s * o[0] + k.c * o[1];
+        const float wx2 = k.c * o[2] - k.s * o[3], wy2 = k.s * o[2] + k.c * o[3], wz2 = o[4];
+        const float inv = rsqrtf(wx2 * wx2 + wy2 * wy2 + wz2 * wz2);
+        const float dz_out = wz2 * inv, I_out = fminf(fmaxf(o[5], 0.f), 1.f);
+        if (live) {
             P.out.px[qi] = ox; P.out.py[qi] = oy;
-            P.out.dx[qi] = wx2 * inv; P.out.dy[qi] = wy2 * inv; P.out.dz[qi] = wz2 * inv;
-            P.out.throughput[qi] = fminf(fmaxf(o[5], 0.f), 1.f);
+            P.out.dx[qi] = wx2 * inv; P.out.dy[qi] = wy2 * inv; P.out.dz[qi] = dz_out;
+            P.out.throughput[qi] = I_out;
             if (P.raw) {
 #pragma unroll
                 for (int d = 0; d < 6; ++d) P.raw[(int64_t)(1 + d) * n + qi] = y[d];
             }
+        }
+        if (P.sc.film) {   // fused splat of the valid outputs (the same floats as written above)
+            const int ch = (live && P.sc.channel) ? (int)P.sc.channel[qi] : 0;
+            splat_warp(P.sc, Gs.wsum + 32 * q, live, ox, oy, dz_out, I_out, ch);
         }
         qhead = (qhead + rows) & (kQueue - 1);
         qcount -= rows;
@@ -692,7 +700,7 @@ int launch_groups(const Params& P, int sms, cudaStream_t stream) {
 }  // namespace
 
 int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams& mp, const plt_rays& in,
-                    const plt_hits& out, float* raw, int64_t n, void* stream) {
+                    const plt_hits& out, float* raw, int64_t n, void* stream, const SplatCtx& sc) {
     if (lay.total_bytes > kMaxImageBytes) return (int)cudaErrorInvalidValue;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -708,6 +716,7 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
     P.lay = lay;
     P.mp = mp;
     P.wimg = (const uint8_t*)d_weights;
+    P.sc = sc;
     static const int groups = [] {
         const char* e = getenv("PLT_MAP_GROUPS");   // tuning knob (4, 6, 7 or 8 tile pipelines per SM)
         return e ? atoi(e) : 8;

@@ -93,14 +93,40 @@ struct MapParams {
 // ---------------------------------------------------------------------------
 // Kernel launchers (implemented in .cu files); return cudaError_t as int.
 // ---------------------------------------------------------------------------
+// Fused sensor splat target (film description folded into kernel constants); film ==
+// nullptr means "no splat".  Device arithmetic: splat_dev.cuh.
+struct SplatCtx {
+    int64_t* film;                 // nullptr: no splat
+    const uint8_t* channel;        // nullable: per-ray channel, indexed by ray index
+    unsigned long long* dropped;   // nullable device counter
+    double W, H, cx, cy;
+    int width, height, channels;
+    float scale;
+    float cxf, cyf, hwf, hhf, sxf, syf;   // fp32 fast-path constants
+};
+
+inline SplatCtx make_splat_ctx(const plt_film_desc& fd, int64_t* film, const uint8_t* channel, float scale,
+                               unsigned long long* dropped) {
+    SplatCtx c;
+    c.film = film; c.channel = channel; c.dropped = dropped;
+    c.W = fd.sensor_w_mm; c.H = fd.sensor_h_mm; c.cx = fd.center_x_mm; c.cy = fd.center_y_mm;
+    c.width = fd.width_px; c.height = fd.height_px; c.channels = fd.channels;
+    c.scale = scale;
+    c.cxf = (float)fd.center_x_mm; c.cyf = (float)fd.center_y_mm;
+    c.hwf = (float)(0.5 * c.W); c.hhf = (float)(0.5 * c.H);
+    c.sxf = (float)(fd.width_px / c.W); c.syf = (float)(fd.height_px / c.H);
+    return c;
+}
+
 int launch_trace_fp32(const Program<float>& pf, const Program<double>& pd, const plt_rays& in,
-                      const plt_hits& out, int64_t n, void* stream);
+                      const plt_hits& out, int64_t n, void* stream, const SplatCtx& sc);
 int launch_trace_fp64(const Program<double>& pd, const plt_rays& in, const plt_hits& out,
-                      int64_t n, void* stream);
+                      int64_t n, void* stream, const SplatCtx& sc);
 int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
                  float scale, int64_t n, unsigned long long* dropped, void* stream);
 int launch_resolve(const plt_film_desc& fd, const int64_t* film, float* out, double scale, void* stream);
 int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams& mp,
-                    const plt_rays& in, const plt_hits& out, float* raw, int64_t n, void* stream);
+                    const plt_rays& in, const plt_hits& out, float* raw, int64_t n, void* stream,
+                    const SplatCtx& sc);
 
 }  // namespace plt

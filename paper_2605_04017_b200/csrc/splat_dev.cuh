@@ -1,0 +1,66 @@
+// splat_dev.cuh -- the per-hit sensor splat as a warp-synchronous device function, shared
+// by the stand-alone splat kernel and the fused query kernels (trace / eval_map epilogues).
+//
+// Eq. 8 accumulates I_out^P * h(x_out^P) * G over the valid paths;
+// Listing 1 adds I_out * dot(w_out, n_cmos) into the pixel of p_out.  With a
+// one-pixel box filter h and G = |w_z|, each valid hit adds
+// llrint(I * |w_z| * scale * 2^32) to film[c][iy][ix].  All arithmetic that decides the
+// pixel and the fixed-point weight is IEEE double with explicit round-to-nearest
+// intrinsics (no FMA contraction) or provably equal to it, so the integer sum is exact,
+// order independent and bit-identical whichever kernel performs it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "plt_internal.h"
+
+namespace plt {
+
+// Pixel key (or -1 with drop = true) and fixed-point weight of one valid hit.
+__device__ __forceinline__ long long splat_key(const SplatCtx& c, float px, float py, float dz, float I, int ch,
+                                               long long& w, bool& drop) {
+    constexpr float kGuard = 2e-3f;
+    // Pixel coordinate: fp32 estimate first.  Its error is < 1e-3 px for any film below
+    // 10^5 px, so when it lies more than kGuard from an integer its floor equals the
+    // floor of the exact double expression of O11; only hits near a pixel edge evaluate
+    // the double expression (bit-exact film).
+    const float fxs = (px - c.cxf + c.hwf) * c.sxf, fys = (c.hhf - (py - c.cyf)) * c.syf;
+    double fxf = floorf(fxs), fyf = floorf(fys);
+    if (fabsf(fxs - rintf(fxs)) < kGuard || fabsf(fys - rintf(fys)) < kGuard) {
+        const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn((double)px, c.cx), c.W * 0.5), c.W), (double)c.width);
+        const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(c.H * 0.5, __dsub_rn((double)py, c.cy)), c.H), (double)c.height);
+        fxf = floor(fx); fyf = floor(fy);
+    }
+    if (fxf >= 0.0 && fxf < (double)c.width && fyf >= 0.0 && fyf < (double)c.height && ch < c.channels) {
+        w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn((double)I, fabs((double)dz)), (double)c.scale), 4294967296.0));
+        return ((long long)ch * c.height + (long long)fyf) * c.width + (long long)fxf;
+    }
+    drop = true;
+    return -1;
+}
+
+// Warp-synchronous splat: ALL 32 lanes call it (hit = false for lanes without a valid
+// hit).  Lanes whose hits share a pixel find each other with __match_any_sync; the lowest
+// lane sums the group's weights through `wsm` (this warp's 32 shared-memory slots) and
+// issues ONE 64-bit atom.add per distinct pixel per warp.
+__device__ __forceinline__ void splat_warp(const SplatCtx& c, long long* wsm, bool hit, float px, float py,
+                                           float dz, float I, int ch) {
+    const int lane = threadIdx.x & 31;
+    long long key = -1, w = 0;
+    bool drop = false;
+    if (hit) key = splat_key(c, px, py, dz, I, ch, w, drop);
+    wsm[lane] = w;
+    __syncwarp();
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && lane == __ffs(peers) - 1) {
+        long long sum = 0;
+        for (unsigned p = peers; p; p &= p - 1) sum += wsm[__ffs(p) - 1];
+        atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)sum);
+    }
+    const unsigned dm = __ballot_sync(0xffffffffu, drop);
+    if (c.dropped && lane == 0 && dm) atomicAdd(c.dropped, (unsigned long long)__popc(dm));
+    __syncwarp();
+}
+
+}  // namespace plt

@@ -26,13 +26,15 @@ def _view(d: dict, lo: int, hi: int) -> dict:
 
 def query_host_batch(lens, path_id: int, m, host_rays: dict, d_rays: dict, h_trace: dict, h_map: dict,
                      film_desc: dict, film, film_host=None, weight_scale: float = 1.0, chunk: int = 1 << 21,
-                     compute_stream=None, copy_stream=None, copy_done=None):
+                     compute_stream=None, copy_stream=None, copy_done=None, fused: bool = True):
     """Trace + map + splat a batch whose inputs are in (pinned) host memory.
 
     host_rays: pinned CPU float32 tensors (RAY_KEYS) + "plane_z"; d_rays / h_trace / h_map:
     device buffers of at least the batch size; film: device int64 film (accumulated, not
     cleared); film_host: optional pinned int64 tensor that receives the film.  chunk must
-    be a multiple of 32 (mask words).  All work is enqueued; nothing synchronises the host.
+    be a multiple of 32 (mask words).  fused: splat inside the query kernels
+    (plt_*_splat) instead of separate plt_splat_sensor launches (bit-identical film).
+    All work is enqueued; nothing synchronises the host.
     """
     import torch
     if chunk % 32:
@@ -53,10 +55,12 @@ def query_host_batch(lens, path_id: int, m, host_rays: dict, d_rays: dict, h_tra
         dv = _view(d_rays, lo, hi)
         dv["plane_z"] = host_rays["plane_z"]
         ht, hm = _view(h_trace, lo, hi), _view(h_map, lo, hi)
-        trace_rays(lens, path_id, dv, ht, stream=cs)
-        eval_map(m, dv, hm, stream=cs)
-        splat_sensor(film_desc, film, ht, weight_scale=weight_scale, stream=cs)
-        splat_sensor(film_desc, film, hm, weight_scale=weight_scale, stream=cs)
+        spl = {"film_desc": film_desc, "film": film, "weight_scale": weight_scale} if fused else None
+        trace_rays(lens, path_id, dv, ht, stream=cs, splat=spl)
+        eval_map(m, dv, hm, stream=cs, splat=spl)
+        if not fused:
+            splat_sensor(film_desc, film, ht, weight_scale=weight_scale, stream=cs)
+            splat_sensor(film_desc, film, hm, weight_scale=weight_scale, stream=cs)
     if film_host is not None:
         with torch.cuda.stream(cs):
             film_host.copy_(film, non_blocking=True)

@@ -131,3 +131,28 @@ def test_compute_calls_fail_loudly_without_gpu(plt):
     assert lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(rays), C.byref(hits), -1, None) == 1
     m = plt.Map(CF.map_blob("C2", 1 << 10))
     assert lib.plt_eval_map(m.handle, C.byref(rays), C.byref(hits), None, 10, None) == 6
+
+
+def test_fused_splat_entry_points_validate_then_fail_loudly(plt):
+    """plt_trace_rays_splat / plt_eval_map_splat: a null target or a bad film description is
+    PLT_E_INVALID_ARG (checked before the device); a valid call needs the GPU (PLT_E_CUDA)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = plt.load()
+    L = plt.Lens(LENSES["dgauss50"])
+    m = plt.Map(CF.map_blob("C2", 1 << 10))
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    rays = plt.Rays(*fake[:6], -5.0)
+    hits = plt.Hits(*fake[:7], None)
+    good = plt.FilmDesc(768, 512, 3, 24.0, 16.0, 0.0, 0.0)
+    bad = plt.FilmDesc(0, 512, 3, 24.0, 16.0, 0.0, 0.0)
+    for fd, want in ((good, 6), (bad, 1)):
+        t = plt.SplatTarget(C.addressof(fd), 8192, None, 1.0, None)
+        assert lib.plt_trace_rays_splat(L.handle, 1 << 10, 0, 0, C.byref(rays), C.byref(hits), C.byref(t), 10,
+                                        None) == want
+        assert lib.plt_eval_map_splat(m.handle, C.byref(rays), C.byref(hits), None, C.byref(t), 10, None) == want
+    assert lib.plt_trace_rays_splat(L.handle, 1 << 10, 0, 0, C.byref(rays), C.byref(hits), None, 10, None) == 1
+    assert lib.plt_eval_map_splat(m.handle, C.byref(rays), C.byref(hits), None, None, 10, None) == 1
+    t = plt.SplatTarget(C.addressof(good), None, None, 1.0, None)     # null film
+    assert lib.plt_eval_map_splat(m.handle, C.byref(rays), C.byref(hits), None, C.byref(t), 10, None) == 1

@@ -13,8 +13,9 @@ FILM = {"width_px": 768, "height_px": 512, "channels": 1, "sensor_w_mm": 36.0, "
         "center_x_mm": 0.0, "center_y_mm": 0.0}
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "separate"])
 @pytest.mark.parametrize("n,chunk", [((1 << 20) + 77, 1 << 18), (5000, 1024), (64, 32)])
-def test_host_batch_matches_device_path(gpu_lib, n, chunk):
+def test_host_batch_matches_device_path(gpu_lib, n, chunk, fused):
     import torch
     from paper_2605_04017_b200.pipeline import query_host_batch
     plt = gpu_lib
@@ -38,7 +39,8 @@ def test_host_batch_matches_device_path(gpu_lib, n, chunk):
     ht2, hm2 = plt.alloc_hits(n), plt.alloc_hits(n)
     film = torch.zeros_like(film_ref)
     film_host = torch.empty(film.numel(), dtype=torch.int64).pin_memory()
-    query_host_batch(lens, pid, m, host, d2, ht2, hm2, FILM, film, film_host, weight_scale=0.5, chunk=chunk)
+    query_host_batch(lens, pid, m, host, d2, ht2, hm2, FILM, film, film_host, weight_scale=0.5, chunk=chunk,
+                     fused=fused)
     torch.cuda.synchronize()
     assert torch.equal(film_host, film_ref.cpu())
     for a, b in ((ht, ht2), (hm, hm2)):
