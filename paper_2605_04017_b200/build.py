@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", *ARCH,
           "-I", os.path.join(HERE, "..", "include")]
 SOURCES = ["lens.cpp", "map.cpp", "abi.cpp", "trace.cu", "splat.cu", "eval_map.cu"]
-HEADERS = ["plt_internal.h", "host.h", "splat_dev.cuh"]
+HEADERS = ["plt_internal.h", "host.h", "splat_dev.cuh", "trace_dev.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -1,0 +1,369 @@
+// trace_dev.cuh -- device code of the float32 trace shared by the ahead-of-time kernels
+// (trace.cu) and the run-time specialised ones (trace_jit.cpp compiles this file with
+// NVRTC after appending a path program baked in as compile-time constants).
+//
+// Packed float32 trace: every thread carries TWO rays in float2 registers, so the ray
+// arithmetic issues as FFMA2 / FMUL2 / FADD2 (one instruction for both rays) while the
+// per-lane work -- comparisons, guard-band tests, MUFU rcp/rsqrt -- addresses the halves
+// of the register pairs directly, and the path program loads, loop control and warp
+// votes are shared by the two rays.  Same operators, order and guard bands as the scalar
+// ray_steps<float> of trace.cu (Eq. 5-7, O4-O8); only the instruction packing differs.
+#pragma once
+
+#ifndef PLT_JIT
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "plt_internal.h"
+#include "splat_dev.cuh"
+#endif
+
+namespace plt {
+
+constexpr float kEpsT = 1e-6f;          // self-hit epsilon, mm
+// Guard bands of the float32 pass: far above
+// the float32 error of an all-T trace (~3e-5 mm, SURVEY [B1]).
+constexpr float kBandEdge = 5e-4f;      // mm, on |rho - a|, sensor edges
+constexpr float kBandKappa = 1e-4f;     // on |kappa| = cos^2(theta_t)
+constexpr float kBandDisc = 1e-5f;      // relative, disc < band * b^2
+constexpr float kBandDir = 1e-4f;       // on |w_z|
+
+struct RayOut { float px, py, dx, dy, dz, I; };
+
+struct Scratch {
+    int* count;   // number of listed rays
+    int* list;    // indices of guard-band rays (capacity n)
+};
+
+__device__ __forceinline__ void write_out(const plt_hits& out, int64_t i, const RayOut& o) {
+    out.px[i] = o.px; out.py[i] = o.py;
+    out.dx[i] = o.dx; out.dy[i] = o.dy; out.dz[i] = o.dz;
+    out.throughput[i] = o.I;
+}
+
+// Warp-aggregated append of guard-band rays to the float64 re-trace list (all lanes call).
+__device__ __forceinline__ void list_append(const Scratch& scr, bool listed, int64_t i, int lane) {
+    const unsigned m = __ballot_sync(0xffffffffu, listed);
+    if (m) {
+        const int leader = __ffs(m) - 1;
+        int pos = 0;
+        if (lane == leader) pos = atomicAdd(scr.count, __popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (listed) scr.list[pos + __popc(m & ((1u << lane) - 1u))] = (int)i;
+    }
+}
+
+constexpr int kBlock = 256;
+
+struct f2 { float2 v; };
+struct m2 { bool x, y; };
+__device__ __forceinline__ f2 mk(float a) { return {make_float2(a, a)}; }
+__device__ __forceinline__ f2 mk(float a, float b) { return {make_float2(a, b)}; }
+__device__ __forceinline__ f2 operator+(f2 a, f2 b) { return {__fadd2_rn(a.v, b.v)}; }
+__device__ __forceinline__ f2 operator-(f2 a, f2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+__device__ __forceinline__ f2 operator-(f2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
+__device__ __forceinline__ f2 operator*(f2 a, f2 b) { return {__fmul2_rn(a.v, b.v)}; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return {__ffma2_rn(a.v, b.v, c.v)}; }
+__device__ __forceinline__ f2 abs2(f2 a) { return {make_float2(fabsf(a.v.x), fabsf(a.v.y))}; }
+__device__ __forceinline__ m2 operator&(m2 a, m2 b) { return {a.x && b.x, a.y && b.y}; }
+__device__ __forceinline__ m2 operator|(m2 a, m2 b) { return {a.x || b.x, a.y || b.y}; }
+__device__ __forceinline__ m2 lt(f2 a, f2 b) { return {a.v.x < b.v.x, a.v.y < b.v.y}; }
+__device__ __forceinline__ m2 le(f2 a, f2 b) { return {a.v.x <= b.v.x, a.v.y <= b.v.y}; }
+__device__ __forceinline__ f2 sel(m2 m, f2 a, f2 b) { return mk(m.x ? a.v.x : b.v.x, m.y ? a.v.y : b.v.y); }
+__device__ __forceinline__ float rcp_approx1(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_approx1(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp1(float b) {                 // Newton-refined, as Math<float>::rcp
+    const float r = rcp_approx1(b);
+    return fmaf(r, fmaf(-b, r, 1.f), r);
+}
+__device__ __forceinline__ f2 rcp_approx2(f2 b) { return mk(rcp_approx1(b.v.x), rcp_approx1(b.v.y)); }
+__device__ __forceinline__ f2 rcp2(f2 b) {                      // Newton-refined, as Math<float>::rcp
+    const f2 r = rcp_approx2(b);
+    return fma2(r, fma2(-b, r, mk(1.f)), r);
+}
+__device__ __forceinline__ f2 sqrt2(f2 x) {                     // as Math<float>::sqrt
+    x = mk(fmaxf(x.v.x, 1e-30f), fmaxf(x.v.y, 1e-30f));
+    const f2 r = mk(rsqrt_approx1(x.v.x), rsqrt_approx1(x.v.y));
+    const f2 s = x * r;
+    return fma2(mk(0.5f) * r, fma2(-s, s, x), s);
+}
+__device__ __forceinline__ f2 rsqrt2(f2 x) {                    // as Math<float>::rsqrt
+    const f2 r = mk(rsqrt_approx1(x.v.x), rsqrt_approx1(x.v.y));
+    return r * fma2(mk(-0.5f) * x * r, r, mk(1.5f));
+}
+__device__ __forceinline__ bool any2(m2 m) { return m.x || m.y; }
+
+__device__ __forceinline__ f2 glass_index2(const Step<float>& st, f2 u, f2 l2) {
+    if (st.gform == kCauchyForm) return fma2(u, fma2(u, mk(st.g[2]), mk(st.g[1])), mk(st.g[0]));
+    f2 s = mk(1.f);
+    s = s + (mk(st.g[0]) * l2) * rcp2(l2 - mk(st.g[3]));
+    s = s + (mk(st.g[1]) * l2) * rcp2(l2 - mk(st.g[4]));
+    s = s + (mk(st.g[2]) * l2) * rcp2(l2 - mk(st.g[5]));
+    return sqrt2(s);
+}
+
+struct Ray2 {
+    f2 ox, oy, oz, wx, wy, wz, I, ncur, u, l2;
+    m2 alive, near;
+};
+
+__device__ __forceinline__ void ray_init2(const Program<float>& P, Ray2& r, m2 alive, f2 ox, f2 oy, float plane_z,
+                                          f2 wx, f2 wy, f2 wz, f2 lam_nm) {
+    if (P.flip) { wz = -wz; plane_z = P.z_mirror - plane_z; }
+    const f2 inv = rsqrt2(fma2(wx, wx, fma2(wy, wy, wz * wz)));
+    r.ox = ox; r.oy = oy; r.oz = mk(plane_z);
+    r.wx = wx * inv; r.wy = wy * inv; r.wz = wz * inv;
+    const f2 lum = lam_nm * mk(1e-3f);
+    r.l2 = lum * lum;
+    r.u = rcp2(r.l2);
+    r.I = mk(1.f); r.ncur = mk(1.f);
+    r.alive = alive; r.near = {false, false};
+}
+
+// One step S_{L_k, sigma_k} of Eq. 5 on a ray pair (O4-O7).  `st` may be a compile-time
+// constant (the JIT-specialised kernels pass literal steps: branches on kind / is_R /
+// glass form and every lens constant fold away) or a __grid_constant__ program entry.
+__device__ __forceinline__ void step2(const Step<float>& st, const Program<float>& P, f2& ox, f2& oy, f2& oz,
+                                      f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
+                                      m2& alive, m2& near) {
+    // O4 direction sanity
+    near = near | (alive & lt(abs2(wz), mk(kBandDir)));
+    alive = alive & lt(mk(0.f), wz * mk(st.sdir));
+    // O5 intersection
+    const f2 lz = oz - mk(st.z);
+    f2 t;
+    if (st.kind != kSphere) {
+        t = -lz * rcp2(wz);
+    } else {
+        const f2 b = fma2(ox, wx, fma2(oy, wy, (lz - mk(st.R)) * wz));
+        const f2 c = fma2(ox, ox, fma2(oy, oy, lz * (lz - mk(st.twoR))));
+        const f2 disc = fma2(b, b, -c);
+        near = near | (alive & lt(disc, (mk(kBandDisc) * b) * b));
+        alive = alive & le(mk(0.f), disc);
+        const f2 rt = sqrt2(disc);
+        // q = b >= 0 ? -b - rt : -b + rt
+        const f2 q = -(b + mk(b.v.x >= 0.f ? rt.v.x : -rt.v.x, b.v.y >= 0.f ? rt.v.y : -rt.v.y));
+        alive = alive & m2{q.v.x != 0.f, q.v.y != 0.f};
+        const f2 t1 = c * rcp2(q);
+        const bool neg_R = st.R < 0.f;
+        const bool cx = (wz.v.x > 0.f) != neg_R, cy = (wz.v.y > 0.f) != neg_R;   // pbrt cap rule (A3)
+        t = mk(cx ? fminf(q.v.x, t1.v.x) : fmaxf(q.v.x, t1.v.x), cy ? fminf(q.v.y, t1.v.y) : fmaxf(q.v.y, t1.v.y));
+    }
+    alive = alive & lt(mk(kEpsT), t);
+    ox = fma2(t, wx, ox); oy = fma2(t, wy, oy); oz = fma2(t, wz, oz);
+    // O6 clear aperture / stop / housing
+    const f2 rho2 = fma2(ox, ox, oy * oy);
+    near = near | (alive & lt(abs2(rho2 - mk(st.a2)), mk(st.band_a)));
+    alive = alive & le(rho2, mk(st.a2));
+    if (P.has_housing) {
+        near = near | (alive & lt(abs2(rho2 - mk(P.housing2)), mk(P.band_h)));
+        alive = alive & le(rho2, mk(P.housing2));
+    }
+    if (st.kind == kStop) return;
+    // O7 interaction (sign of the normal folded into g, as in ray_steps)
+    f2 nx, ny, nz;
+    if (st.kind == kSphere) { nx = ox * mk(st.invR); ny = oy * mk(st.invR); nz = fma2(oz - mk(st.z), mk(st.invR), mk(-1.f)); }
+    else { nx = mk(0.f); ny = mk(0.f); nz = mk(1.f); }
+    const f2 wn = fma2(nx, wx, fma2(ny, wy, nz * wz));
+    const f2 cosi = abs2(wn);
+    const f2 n2 = glass_index2(st, u, l2);
+    const f2 eta = ncur * rcp2(n2);
+    const f2 kappa = fma2(-(eta * eta), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
+    near = near | (alive & lt(abs2(kappa), mk(kBandKappa)));
+    const f2 cost = sqrt2(mk(fmaxf(kappa.v.x, 0.f), fmaxf(kappa.v.y, 0.f)));
+    const f2 A = ncur * cosi, B = n2 * cost, C = n2 * cosi, D = ncur * cost;
+    const f2 ApB = A + B, CpD = C + D;
+    const f2 inv = rcp_approx2(ApB * CpD);
+    const f2 rs = ((A - B) * CpD) * inv, rp = ((C - D) * ApB) * inv;
+    const f2 Rf0 = mk(0.5f) * fma2(rs, rs, rp * rp);
+    const m2 tir = lt(kappa, mk(0.f));
+    const f2 Rf = sel(tir, mk(1.f), Rf0);
+    if (!st.is_R) {
+        alive = alive & m2{!tir.x, !tir.y};   // TIR on a T step absorbs (A6)
+        const f2 g0 = fma2(eta, cosi, -cost);
+        const f2 g = mk(wn.v.x > 0.f ? -g0.v.x : g0.v.x, wn.v.y > 0.f ? -g0.v.y : g0.v.y);
+        wx = fma2(eta, wx, g * nx); wy = fma2(eta, wy, g * ny); wz = fma2(eta, wz, g * nz);
+        I = fma2(-I, Rf, I);
+        ncur = n2;
+    } else {
+        const f2 two_wn = wn + wn;
+        wx = fma2(-two_wn, nx, wx); wy = fma2(-two_wn, ny, wy); wz = fma2(-two_wn, nz, wz);
+        I = I * Rf;
+    }
+}
+
+// Steps [s0, s1) of the program (the generic, runtime-indexed path).  The warp leaves the
+// loop once every lane is dead (warp-uniform; no divergent exits).
+__device__ __forceinline__ void ray_steps2(const Program<float>& P, Ray2& r, int s0, int s1) {
+    f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;
+    m2 alive = r.alive, near = r.near;
+    for (int s = s0; s < s1; ++s) {
+        if (!__any_sync(0xffffffffu, any2(alive))) break;
+        step2(P.st[s], P, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near);
+    }
+    r.ox = ox; r.oy = oy; r.oz = oz; r.wx = wx; r.wy = wy; r.wz = wz; r.I = I; r.ncur = ncur;
+    r.alive = alive; r.near = near;
+}
+
+// Step policy of the generic kernel: phases [0, split) and [split, n_steps) of P.
+struct GenericSteps {
+    __device__ __forceinline__ static bool compact(const Program<float>& P) {
+        return P.split > 0 && P.split < P.n_steps;
+    }
+    __device__ __forceinline__ static void run(const Program<float>& P, Ray2& r, int phase) {
+        const bool c = compact(P);
+        if (phase == 0) ray_steps2(P, r, 0, c ? P.split : P.n_steps);
+        else ray_steps2(P, r, P.split, P.n_steps);
+    }
+};
+
+// O8 for one lane of the pair (cheap; scalar keeps it simple).
+__device__ __forceinline__ bool ray_finish1(const Program<float>& P, bool alive, bool& near, float ox, float oy,
+                                            float oz, float wx, float wy, float wz, float I, RayOut& out) {
+    near |= alive && fabsf(wz) < kBandDir;
+    alive = alive && wz > 0.f;
+    const float t = (P.z_out - oz) * rcp1(wz);
+    alive = alive && t > 0.f;
+    const float px = fmaf(t, wx, ox), py = fmaf(t, wy, oy);
+    if (P.has_rect) {
+        const float ex = fabsf(px - P.rect_cx) - P.rect_hw, ey = fabsf(py - P.rect_cy) - P.rect_hh;
+        near |= alive && (fabsf(ex) < kBandEdge || fabsf(ey) < kBandEdge);
+        alive = alive && ex <= 0.f && ey <= 0.f;
+    }
+    if (alive) out = RayOut{px, py, wx, wy, P.flip ? -wz : wz, I};
+    else out = RayOut{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    return alive;
+}
+
+// Main pass, packed: a block owns 512 consecutive rays (thread t: rays base + t and
+// base + 256 + t, so loads stay 128-byte coalesced).  Compaction after step `split` puts
+// the survivors into slots 0..S-1 and thread t continues with slots 2t and 2t + 1.
+template <class Steps>
+__device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt_rays& in, const plt_hits& out,
+                                              int64_t n, const Scratch& scr, const SplatCtx& sc) {
+    constexpr int kRays = 2 * kBlock;
+    __shared__ float sm_v[8][kRays];       // ox oy oz wx wy wz I ncur of the survivors
+    __shared__ float sm_lam[kRays];
+    __shared__ int sm_idx[kRays];
+    __shared__ unsigned sm_mask[kRays / 32];
+    __shared__ int sm_wcnt[kBlock / 32];
+    __shared__ long long sm_w[kBlock];     // fused splat: per-warp aggregation slots
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool compact = Steps::compact(P);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (tid < kRays / 32) sm_mask[tid] = 0u;
+    __syncthreads();
+    for (int64_t base = (int64_t)blockIdx.x * kRays; base < n; base += (int64_t)gridDim.x * kRays) {
+        int64_t ix = base + tid, iy = base + kBlock + tid;
+        const m2 in_range{ix < n, iy < n};
+        float v[2][6] = {{0.f, 0.f, 0.f, 0.f, 1.f, 550.f}, {0.f, 0.f, 0.f, 0.f, 1.f, 550.f}};
+        if (in_range.x) {
+            v[0][0] = __ldg(in.ox + ix); v[0][1] = __ldg(in.oy + ix); v[0][2] = __ldg(in.dx + ix);
+            v[0][3] = __ldg(in.dy + ix); v[0][4] = __ldg(in.dz + ix); v[0][5] = __ldg(in.lambda_nm + ix);
+        }
+        if (in_range.y) {
+            v[1][0] = __ldg(in.ox + iy); v[1][1] = __ldg(in.oy + iy); v[1][2] = __ldg(in.dx + iy);
+            v[1][3] = __ldg(in.dy + iy); v[1][4] = __ldg(in.dz + iy); v[1][5] = __ldg(in.lambda_nm + iy);
+        }
+        f2 lam = mk(v[0][5], v[1][5]);
+        Ray2 r;
+        ray_init2(P, r, in_range, mk(v[0][0], v[1][0]), mk(v[0][1], v[1][1]), in.plane_z_mm, mk(v[0][2], v[1][2]),
+                  mk(v[0][3], v[1][3]), mk(v[0][4], v[1][4]), lam);
+        Steps::run(P, r, 0);
+        m2 own = in_range;
+        int slot_x = tid, slot_y = kBlock + tid;   // position within the block's 512 rays
+        if (compact) {
+            const RayOut zero{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (in_range.x && !r.alive.x) { write_out(out, ix, zero); if (out.flags) out.flags[ix] = (uint8_t)r.near.x; }
+            if (in_range.y && !r.alive.y) { write_out(out, iy, zero); if (out.flags) out.flags[iy] = (uint8_t)r.near.y; }
+            list_append(scr, in_range.x && !r.alive.x && r.near.x, ix, lane);
+            list_append(scr, in_range.y && !r.alive.y && r.near.y, iy, lane);
+            const unsigned lx = __ballot_sync(0xffffffffu, r.alive.x), ly = __ballot_sync(0xffffffffu, r.alive.y);
+            if (lane == 0) sm_wcnt[warp] = __popc(lx) + __popc(ly);
+            __syncthreads();
+            int before = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < kBlock / 32; ++w) { const int c = sm_wcnt[w]; before += w < warp ? c : 0; total += c; }
+            auto put = [&](int slot, float a0, float a1, float a2, float a3, float a4, float a5, float a6, float a7,
+                           float lm, int code) {
+                sm_v[0][slot] = a0; sm_v[1][slot] = a1; sm_v[2][slot] = a2; sm_v[3][slot] = a3;
+                sm_v[4][slot] = a4; sm_v[5][slot] = a5; sm_v[6][slot] = a6; sm_v[7][slot] = a7;
+                sm_lam[slot] = lm; sm_idx[slot] = code;
+            };
+            if (r.alive.x)
+                put(before + __popc(lx & lt_mask), r.ox.v.x, r.oy.v.x, r.oz.v.x, r.wx.v.x, r.wy.v.x, r.wz.v.x, r.I.v.x,
+                    r.ncur.v.x, lam.v.x, tid | (r.near.x ? 0x10000 : 0));
+            if (r.alive.y)
+                put(before + __popc(lx) + __popc(ly & lt_mask), r.ox.v.y, r.oy.v.y, r.oz.v.y, r.wx.v.y, r.wy.v.y,
+                    r.wz.v.y, r.I.v.y, r.ncur.v.y, lam.v.y, (kBlock + tid) | (r.near.y ? 0x10000 : 0));
+            __syncthreads();
+            own = m2{2 * tid < total, 2 * tid + 1 < total};
+            if (own.x) {
+                auto ld2 = [&](int k) { const float2 p = *reinterpret_cast<const float2*>(&sm_v[k][2 * tid]); return f2{p}; };
+                r.ox = ld2(0); r.oy = ld2(1); r.oz = ld2(2); r.wx = ld2(3); r.wy = ld2(4); r.wz = ld2(5);
+                r.I = ld2(6); r.ncur = ld2(7);
+                const float2 lm = *reinterpret_cast<const float2*>(&sm_lam[2 * tid]);
+                const int2 code = *reinterpret_cast<const int2*>(&sm_idx[2 * tid]);
+                lam = f2{lm};
+                if (!own.y) { lam.v.y = 550.f; r.wz.v.y = 1.f; }   // idle lane: harmless finite state
+                const f2 lum = lam * mk(1e-3f);
+                r.l2 = lum * lum;
+                r.u = rcp2(r.l2);
+                r.near = m2{(code.x & 0x10000) != 0, own.y && (code.y & 0x10000) != 0};
+                slot_x = code.x & 0xFFFF;
+                slot_y = own.y ? (code.y & 0xFFFF) : 0;
+                ix = base + slot_x;
+                iy = base + slot_y;
+            }
+            r.alive = own;
+            Steps::run(P, r, 1);
+        }
+        RayOut ox_, oy_;
+        bool nx = r.near.x, ny = r.near.y;
+        const bool vx = ray_finish1(P, r.alive.x, nx, r.ox.v.x, r.oy.v.x, r.oz.v.x, r.wx.v.x, r.wy.v.x, r.wz.v.x, r.I.v.x, ox_);
+        const bool vy = ray_finish1(P, r.alive.y, ny, r.ox.v.y, r.oy.v.y, r.oz.v.y, r.wx.v.y, r.wy.v.y, r.wz.v.y, r.I.v.y, oy_);
+        if (own.x) {
+            write_out(out, ix, ox_);
+            if (out.flags) out.flags[ix] = (uint8_t)nx;
+            if (vx) atomicOr(&sm_mask[slot_x >> 5], 1u << (slot_x & 31));
+        }
+        if (own.y) {
+            write_out(out, iy, oy_);
+            if (out.flags) out.flags[iy] = (uint8_t)ny;
+            if (vy) atomicOr(&sm_mask[slot_y >> 5], 1u << (slot_y & 31));
+        }
+        list_append(scr, own.x && nx, ix, lane);
+        list_append(scr, own.y && ny, iy, lane);
+        if (sc.film) {   // fused splat; guard-band rays are splatted by the fp64 refine instead
+            const int cx = (own.x && sc.channel) ? (int)sc.channel[ix] : 0;
+            const int cy = (own.y && sc.channel) ? (int)sc.channel[iy] : 0;
+            splat_warp(sc, sm_w + 32 * warp, own.x && vx && !nx, ox_.px, ox_.py, ox_.dz, ox_.I, cx);
+            splat_warp(sc, sm_w + 32 * warp, own.y && vy && !ny, oy_.px, oy_.py, oy_.dz, oy_.I, cy);
+        }
+        __syncthreads();
+        if (tid < kRays / 32) {
+            if (base + 32 * tid < n) out.mask_bits[(base >> 5) + tid] = sm_mask[tid];
+            sm_mask[tid] = 0u;
+        }
+        __syncthreads();   // sm_* reused by the next iteration
+    }
+}
+
+#ifndef PLT_JIT
+// The generic packed kernel (runtime path program).
+__global__ void __launch_bounds__(kBlock) trace_kernel_x2(const __grid_constant__ Program<float> P, plt_rays in,
+                                                          plt_hits out, int64_t n, Scratch scr,
+                                                          const __grid_constant__ SplatCtx sc) {
+    trace_x2_body<GenericSteps>(P, in, out, n, scr, sc);
+}
+#endif
+
+}  // namespace plt
