@@ -246,6 +246,16 @@ PLT_API plt_status plt_trace_rays_splat(const plt_lens* lens, uint64_t path_id, 
 PLT_API plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out,
                                       const plt_splat_target* splat, int64_t n, void* cuda_stream);
 
+/*
+ * Inspection: the sm_100a cubin of the float32 trace kernel specialised for this path
+ * program (the kernel plt_trace_rays launches for large batches; compiled with NVRTC, no
+ * GPU needed).  Two-call pattern: *size receives the cubin size; the bytes are written
+ * when buf != NULL and capacity >= size.  Errors: PLT_E_UNSUPPORTED (NVRTC unavailable),
+ * PLT_E_VALIDATION (compilation failed; plt_last_error holds the log), PLT_E_CAPACITY.
+ */
+PLT_API plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir dir, void* buf,
+                                       size_t capacity, size_t* size);
+
 /* out[i] = film[i] * 2^-32 * scale (float), for channels*height*width pixels. */
 PLT_API plt_status plt_film_resolve(const plt_film_desc* film_desc, const int64_t* film, float* out,
                             double scale, void* cuda_stream);

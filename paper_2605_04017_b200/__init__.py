@@ -28,7 +28,8 @@ _STATUS = {0: "PLT_OK", 1: "PLT_E_INVALID_ARG", 2: "PLT_E_PARSE", 3: "PLT_E_VALI
 
 EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "plt_lens_info",
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
-            "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat")
+            "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
+            "plt_trace_jit_cubin")
 
 
 class PltError(RuntimeError):
@@ -93,9 +94,10 @@ def load():
     L.plt_film_resolve.argtypes = [p, p, p, d, p]
     L.plt_trace_rays_splat.argtypes = [p, u64, i, i, p, p, p, i64, p]
     L.plt_eval_map_splat.argtypes = [p, p, p, p, p, i64, p]
+    L.plt_trace_jit_cubin.argtypes = [p, u64, i, p, C.c_size_t, C.POINTER(C.c_size_t)]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
-              "plt_eval_map_splat"):
+              "plt_eval_map_splat", "plt_trace_jit_cubin"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -149,6 +151,15 @@ class Lens:
         ij = (C.c_int32 * (2 * cnt.value))()
         _check(L.plt_enumerate_ghosts(self._h, max_bounces, min_throughput, ids, ij, cnt.value, C.byref(cnt)))
         return list(ids), [(ij[2 * k], ij[2 * k + 1]) for k in range(cnt.value)]
+
+    def trace_jit_cubin(self, path_id: int, direction: int = 0) -> bytes:
+        """plt_trace_jit_cubin: the sm_100a cubin of the trace kernel specialised for this path."""
+        L = load()
+        size = C.c_size_t()
+        _check(L.plt_trace_jit_cubin(self._h, int(path_id), direction, None, 0, C.byref(size)))
+        buf = C.create_string_buffer(size.value)
+        _check(L.plt_trace_jit_cubin(self._h, int(path_id), direction, buf, size.value, C.byref(size)))
+        return buf.raw[:size.value]
 
     def all_t_id(self) -> int:
         return 1 << self.info()["n_optical"]

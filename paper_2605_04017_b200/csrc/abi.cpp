@@ -238,6 +238,24 @@ plt_status plt_splat_sensor(const plt_film_desc* fd, int64_t* film, const plt_hi
     PLT_GUARD_END
 }
 
+plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir dir, void* buf, size_t capacity,
+                               size_t* size) {
+    PLT_GUARD_BEGIN
+    if (!lens || !size) return set_err(PLT_E_INVALID_ARG, "lens and size must be non-null");
+    if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
+    auto cp = plt::compile_path(*lens, path_id, (int)dir);
+    std::string log;
+    const std::string cubin = plt::trace_jit_cubin(cp->pf, &log);
+    if (cubin.empty())
+        return log.empty() ? set_err(PLT_E_UNSUPPORTED, "NVRTC is not available")
+                           : set_err(PLT_E_VALIDATION, "trace JIT compilation failed: " + log);
+    *size = cubin.size();
+    if (!buf || capacity < cubin.size()) return buf ? set_err(PLT_E_CAPACITY, "buffer too small") : PLT_OK;
+    std::memcpy(buf, cubin.data(), cubin.size());
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
 plt_status plt_film_resolve(const plt_film_desc* fd, const int64_t* film, float* out, double scale, void* cuda_stream) {
     PLT_GUARD_BEGIN
     if (!fd || !film || !out) return set_err(PLT_E_INVALID_ARG, "null film/out");

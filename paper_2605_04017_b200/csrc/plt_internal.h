@@ -122,6 +122,15 @@ int launch_trace_fp32(const Program<float>& pf, const Program<double>& pd, const
                       const plt_hits& out, int64_t n, void* stream, const SplatCtx& sc);
 int launch_trace_fp64(const Program<double>& pd, const plt_rays& in, const plt_hits& out,
                       int64_t n, void* stream, const SplatCtx& sc);
+// Run-time specialised packed trace kernel for P (trace_jit.cpp): cudaKernel_t or nullptr.
+void* trace_jit_kernel(const Program<float>& P);
+#ifndef PLT_JIT
+}  // namespace plt
+#include <string>
+namespace plt {
+// The specialised kernel's cubin compiled without a GPU ("" on failure; log in *log_out).
+std::string trace_jit_cubin(const Program<float>& P, std::string* log_out);
+#endif
 int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
                  float scale, int64_t n, unsigned long long* dropped, void* stream);
 int launch_resolve(const plt_film_desc& fd, const int64_t* film, float* out, double scale, void* stream);

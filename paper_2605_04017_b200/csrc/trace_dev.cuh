@@ -131,7 +131,8 @@ __device__ __forceinline__ void ray_init2(const Program<float>& P, Ray2& r, m2 a
 // One step S_{L_k, sigma_k} of Eq. 5 on a ray pair (O4-O7).  `st` may be a compile-time
 // constant (the JIT-specialised kernels pass literal steps: branches on kind / is_R /
 // glass form and every lens constant fold away) or a __grid_constant__ program entry.
-__device__ __forceinline__ void step2(const Step<float>& st, const Program<float>& P, f2& ox, f2& oy, f2& oz,
+template <class PP>   // Program<float>, or the JIT's constexpr header (has_housing, housing2, band_h)
+__device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox, f2& oy, f2& oz,
                                       f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
                                       m2& alive, m2& near) {
     // O4 direction sanity

@@ -1,0 +1,226 @@
+// trace_jit.cpp -- run-time specialisation of the packed float32 trace for one path program.
+//
+// The generic kernel (trace_kernel_x2) reads every step of the path program from the
+// __grid_constant__ parameter inside the step loop: ~20 uniform constant loads, a loop
+// counter and branches on the surface kind / interaction / glass form per step.  For a
+// given (lens, path, direction) all of that is known on the host, so this module emits a
+// kernel whose steps are literal compile-time constants -- the step loop is unrolled,
+// the branches and loads fold away and lens constants become instruction immediates --
+// and compiles it with NVRTC for sm_100a on first use (cached per program).  The device
+// code is the same trace_dev.cuh the ahead-of-time kernels use; only the step policy
+// differs.  NVRTC is loaded with dlopen: if it is missing, or compilation fails, the call
+// uses the generic kernel (the same GPU computation, never a CPU path).
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "plt_internal.h"
+
+namespace plt {
+
+namespace {
+
+#include "jit_sources.inc"   // kJitSources[]: plt.h, plt_internal.h, splat_dev.cuh, trace_dev.cuh (no #includes)
+
+struct Nvrtc {
+    bool ok = false;
+    decltype(&nvrtcCreateProgram) create = nullptr;
+    decltype(&nvrtcCompileProgram) compile = nullptr;
+    decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+    decltype(&nvrtcGetCUBIN) cubin = nullptr;
+    decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+    decltype(&nvrtcGetProgramLog) log = nullptr;
+    decltype(&nvrtcDestroyProgram) destroy = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+    static Nvrtc n = [] {
+        Nvrtc r;
+        const char* env = std::getenv("PLT_NVRTC");
+        const char* names[] = {env ? env : "libnvrtc.so.12", "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                               "/usr/local/cuda/lib64/libnvrtc.so"};
+        void* h = nullptr;
+        for (const char* nm : names)
+            if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+        if (!h) return r;
+        r.create = (decltype(r.create))dlsym(h, "nvrtcCreateProgram");
+        r.compile = (decltype(r.compile))dlsym(h, "nvrtcCompileProgram");
+        r.cubin_size = (decltype(r.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+        r.cubin = (decltype(r.cubin))dlsym(h, "nvrtcGetCUBIN");
+        r.log_size = (decltype(r.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+        r.log = (decltype(r.log))dlsym(h, "nvrtcGetProgramLog");
+        r.destroy = (decltype(r.destroy))dlsym(h, "nvrtcDestroyProgram");
+        r.ok = r.create && r.compile && r.cubin_size && r.cubin && r.log_size && r.log && r.destroy;
+        return r;
+    }();
+    return n;
+}
+
+// Exact float literal (hexadecimal significand; C++17).
+std::string lit(float v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%af", (double)v);
+    return b;
+}
+
+const char* kPrelude =
+    "#define PLT_JIT 1\n"
+    "typedef signed char int8_t; typedef unsigned char uint8_t;\n"
+    "typedef short int16_t; typedef unsigned short uint16_t;\n"
+    "typedef int int32_t; typedef unsigned int uint32_t;\n"
+    "typedef long long int64_t; typedef unsigned long long uint64_t;\n";
+
+std::string gen_phase(const Program<float>& P, int s0, int s1) {
+    std::string c = "        do {\n";
+    for (int s = s0; s < s1; ++s) {
+        const Step<float>& st = P.st[s];
+        c += "            if (!__any_sync(0xffffffffu, any2(alive))) break;\n";
+        c += "            { constexpr Step<float> st{" + lit(st.z) + ", " + lit(st.R) + ", " + lit(st.twoR) + ", " +
+             lit(st.invR) + ", " + lit(st.a2) + ", " + lit(st.band_a) + ", " + lit(st.sdir) + ", {";
+        for (int k = 0; k < 6; ++k) c += lit(st.g[k]) + (k < 5 ? ", " : "");
+        c += "}, " + std::to_string(st.kind) + ", " + std::to_string(st.is_R) + ", " + std::to_string(st.gform) +
+             ", 0};\n              step2(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+    }
+    c += "        } while (0);\n";
+    return c;
+}
+
+int jit_min_blocks() {   // blocks per SM the specialised kernel is register-limited to (tuning knob)
+    static const int v = [] {
+        const char* e = std::getenv("PLT_JIT_MINB");
+        return e ? std::atoi(e) : 4;
+    }();
+    return v;
+}
+
+std::string gen_source(const Program<float>& P) {
+    const bool compact = P.split > 0 && P.split < P.n_steps;
+    std::string src = kPrelude;
+    src += "#define PLT_JIT_MINB " + std::to_string(jit_min_blocks()) + "\n";
+    for (const char* part : kJitSources) src += part;
+    src += "\nnamespace plt {\nstruct JitSteps {\n"
+           "    __device__ __forceinline__ static bool compact(const Program<float>&) { return ";
+    src += compact ? "true" : "false";
+    src += "; }\n    struct Hdr { int has_housing; float housing2, band_h; };\n"
+           "    __device__ __forceinline__ static void run(const Program<float>&, Ray2& r, int phase) {\n"
+           "        constexpr Hdr H{" + std::to_string(P.has_housing) + ", " + lit(P.housing2) + ", " + lit(P.band_h) +
+           "};\n"
+           "        f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;\n"
+           "        m2 alive = r.alive, near = r.near;\n        if (phase == 0) {\n";
+    src += gen_phase(P, 0, compact ? P.split : P.n_steps);
+    src += "        } else {\n";
+    src += gen_phase(P, compact ? P.split : P.n_steps, P.n_steps);
+    src += "        }\n"
+           "        r.ox = ox; r.oy = oy; r.oz = oz; r.wx = wx; r.wy = wy; r.wz = wz; r.I = I; r.ncur = ncur;\n"
+           "        r.alive = alive; r.near = near;\n    }\n};\n}  // namespace plt\n"
+           "extern \"C\" __global__ void __launch_bounds__(256, PLT_JIT_MINB) plt_trace_jit(\n"
+           "        const __grid_constant__ plt::Program<float> P, plt_rays in, plt_hits out, int64_t n,\n"
+           "        plt::Scratch scr, const __grid_constant__ plt::SplatCtx sc) {\n"
+           "    plt::trace_x2_body<plt::JitSteps>(P, in, out, n, scr, sc);\n}\n";
+    return src;
+}
+
+struct Entry {
+    bool tried = false;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kernel = nullptr;
+};
+
+std::mutex g_mu;
+std::map<std::string, Entry> g_cache;
+
+std::string key_of(const Program<float>& P) {
+    const size_t bytes = offsetof(Program<float>, st) + sizeof(Step<float>) * (size_t)P.n_steps;
+    return std::string(reinterpret_cast<const char*>(&P), bytes);
+}
+
+bool verbose() {
+    static const bool v = std::getenv("PLT_JIT_VERBOSE") != nullptr;
+    return v;
+}
+
+}  // namespace
+
+std::string trace_jit_source(const Program<float>& P) { return gen_source(P); }
+
+// Compile (or fetch) the specialised kernel for P; nullptr if unavailable.
+void* trace_jit_kernel(const Program<float>& P) {
+    static const bool off = [] {
+        const char* e = std::getenv("PLT_TRACE_JIT");
+        return e && std::strcmp(e, "0") == 0;
+    }();
+    if (off || P.n_steps <= 0) return nullptr;
+    const std::string key = key_of(P);
+    std::lock_guard<std::mutex> g(g_mu);
+    Entry& e = g_cache[key];
+    if (e.tried) return (void*)e.kernel;
+    e.tried = true;
+    const Nvrtc& nv = nvrtc();
+    if (!nv.ok) {
+        if (verbose()) std::fprintf(stderr, "plt: NVRTC not found; generic trace kernel\n");
+        return nullptr;
+    }
+    const std::string src = gen_source(P);
+    nvrtcProgram prog;
+    if (nv.create(&prog, src.c_str(), "plt_trace_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return nullptr;
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=true", "-default-device"};
+    const nvrtcResult rc = nv.compile(prog, 5, opts);
+    if (rc != NVRTC_SUCCESS || verbose()) {
+        size_t ls = 0;
+        nv.log_size(prog, &ls);
+        std::vector<char> log(ls + 1, 0);
+        nv.log(prog, log.data());
+        if (rc != NVRTC_SUCCESS || ls > 1)
+            std::fprintf(stderr, "plt: trace JIT %s:\n%s\n", rc == NVRTC_SUCCESS ? "log" : "FAILED", log.data());
+    }
+    if (rc != NVRTC_SUCCESS) { nv.destroy(&prog); return nullptr; }
+    size_t cs = 0;
+    nv.cubin_size(prog, &cs);
+    std::vector<char> cubin(cs);
+    nv.cubin(prog, cubin.data());
+    nv.destroy(&prog);
+    if (cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&e.kernel, e.lib, "plt_trace_jit") != cudaSuccess) {
+        cudaGetLastError();
+        e.kernel = nullptr;
+        return nullptr;
+    }
+    if (verbose()) std::fprintf(stderr, "plt: trace JIT compiled (%zu-byte cubin, %d steps)\n", cs, P.n_steps);
+    return (void*)e.kernel;
+}
+
+// Compile P's kernel to a cubin without a GPU (tests / inspection); "" on failure.
+std::string trace_jit_cubin(const Program<float>& P, std::string* log_out) {
+    const Nvrtc& nv = nvrtc();
+    if (!nv.ok) return {};
+    const std::string src = gen_source(P);
+    nvrtcProgram prog;
+    if (nv.create(&prog, src.c_str(), "plt_trace_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return {};
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=true", "-default-device"};
+    const nvrtcResult rc = nv.compile(prog, 5, opts);
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    nv.log(prog, &log[0]);
+    if (log_out) *log_out = log;
+    std::string out;
+    if (rc == NVRTC_SUCCESS) {
+        size_t cs = 0;
+        nv.cubin_size(prog, &cs);
+        out.resize(cs);
+        nv.cubin(prog, &out[0]);
+    }
+    nv.destroy(&prog);
+    return out;
+}
+
+}  // namespace plt

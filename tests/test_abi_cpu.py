@@ -156,3 +156,13 @@ def test_fused_splat_entry_points_validate_then_fail_loudly(plt):
     assert lib.plt_eval_map_splat(m.handle, C.byref(rays), C.byref(hits), None, None, 10, None) == 1
     t = plt.SplatTarget(C.addressof(good), None, None, 1.0, None)     # null film
     assert lib.plt_eval_map_splat(m.handle, C.byref(rays), C.byref(hits), None, C.byref(t), 10, None) == 1
+
+
+@pytest.mark.parametrize("name,path,direction", [("C1", 0, 0), ("C2", 0, 0), ("C3", 0, 1), ("C4_22", 65616, 0)])
+def test_trace_jit_compiles_without_gpu(plt, name, path, direction):
+    """plt_trace_jit_cubin: the path-specialised trace kernel compiles with NVRTC for sm_100a
+    on the build host (catches a broken JIT source before any GPU run)."""
+    cfg = CF.CONFIGS[name]
+    L = plt.Lens(CF.lens_text(name), **cfg["opts"])
+    cubin = L.trace_jit_cubin(path or L.all_t_id(), direction)
+    assert cubin[:4] == b"\x7fELF" and b"plt_trace_jit" in cubin

@@ -1,0 +1,51 @@
+"""The run-time specialised trace kernel (trace_jit.cpp, used for all-T paths) against the
+generic packed kernel (PLT_TRACE_JIT=0, run in a subprocess since the switch is read once
+per process): identical masks and guard-band flags, outputs equal to float32 rounding.
+Both are parity-checked against the oracle elsewhere (test_gpu_trace.py runs the JIT for
+all-T paths and the generic kernel for ghost paths)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from plt_inputs import configs as C
+from plt_inputs import rays as R
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_jit_matches_generic_kernel(gpu_lib, tmp_path, name):
+    import torch
+    plt = gpu_lib
+    out = tmp_path / "generic.npz"
+    code = f"""
+import sys; sys.path.insert(0, {ROOT!r})
+import numpy as np, torch
+import paper_2605_04017_b200 as plt
+from plt_inputs import configs as C, rays as R
+cfg = C.CONFIGS[{name!r}]
+lens = plt.Lens(C.lens_text({name!r}), **cfg["opts"])
+d = plt.rays_to_device(R.gen_rays(cfg["law"], 17, 0, (1 << 18) + 5))
+h = plt.alloc_hits((1 << 18) + 5, flags=True)
+plt.trace_rays(lens, lens.all_t_id(), d, h, direction=cfg["direction"])
+torch.cuda.synchronize()
+np.savez({str(out)!r}, **{{k: h[k].cpu().numpy() for k in plt.HIT_KEYS + ("mask_bits", "flags")}})
+"""
+    env = dict(os.environ, PLT_TRACE_JIT="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+    g = np.load(out)
+    cfg = C.CONFIGS[name]
+    lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+    n = (1 << 18) + 5
+    d = plt.rays_to_device(R.gen_rays(cfg["law"], 17, 0, n))
+    h = plt.alloc_hits(n, flags=True)
+    plt.trace_rays(lens, lens.all_t_id(), d, h, direction=cfg["direction"])
+    torch.cuda.synchronize()
+    assert np.array_equal(h["mask_bits"].cpu().numpy(), g["mask_bits"])
+    assert np.array_equal(h["flags"].cpu().numpy(), g["flags"])
+    for k, tol in (("px", 1e-5), ("py", 1e-5), ("dx", 1e-6), ("dy", 1e-6), ("dz", 1e-6), ("throughput", 1e-6)):
+        assert np.max(np.abs(h[k].cpu().numpy() - g[k])) <= tol, k
