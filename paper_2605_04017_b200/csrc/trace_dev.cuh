@@ -137,7 +137,11 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
                                       m2& alive, m2& near) {
     // O4 direction sanity
     near = near | (alive & lt(abs2(wz), mk(kBandDir)));
+#ifdef PLT_JIT   // constant program: the sign test and the air shortcut below fold at compile time
+    alive = alive & (st.sdir > 0.f ? lt(mk(0.f), wz) : lt(wz, mk(0.f)));   // w_z * sdir > 0, sdir = +-1
+#else
     alive = alive & lt(mk(0.f), wz * mk(st.sdir));
+#endif
     // O5 intersection
     const f2 lz = oz - mk(st.z);
     f2 t;
@@ -175,8 +179,14 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     else { nx = mk(0.f); ny = mk(0.f); nz = mk(1.f); }
     const f2 wn = fma2(nx, wx, fma2(ny, wy, nz * wz));
     const f2 cosi = abs2(wn);
-    const f2 n2 = glass_index2(st, u, l2);
-    const f2 eta = ncur * rcp2(n2);
+    // air on the far side (constant n = 1): n2 = 1 and eta = ncur exactly
+#ifdef PLT_JIT
+    const bool air = st.gform == kCauchyForm && st.g[0] == 1.f && st.g[1] == 0.f && st.g[2] == 0.f;
+#else
+    constexpr bool air = false;
+#endif
+    const f2 n2 = air ? mk(1.f) : glass_index2(st, u, l2);
+    const f2 eta = air ? ncur : ncur * rcp2(n2);
     const f2 kappa = fma2(-(eta * eta), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
     near = near | (alive & lt(abs2(kappa), mk(kBandKappa)));
     const f2 cost = sqrt2(mk(fmaxf(kappa.v.x, 0.f), fmaxf(kappa.v.y, 0.f)));
