@@ -48,7 +48,11 @@ constexpr uint32_t kMaxImageBytes = 20480;
 
 struct GroupSmem {
     alignas(16) float stage[2][kNumIn][kTile];  // TMA-staged ray inputs
-    int qi[kQueue];                          // queued valid ray indices
+    // queue of valid rays, kept with their canonical inputs so the regressor neither
+    // gathers the inputs again nor re-canonicalises them (SoA: conflict-free)
+    float qx[4][kQueue];                     // normalised canonical inputs x
+    float qc[kQueue], qs[kQueue];            // rotation (cos, sin) to undo
+    int qi[kQueue];                          // ray index | reflection flag << 31
     int wcount[4];                           // per-warp valid counts (prefix)
     long long wsum[kTile];                   // fused splat: per-warp aggregation slots
 };
@@ -545,13 +549,21 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         group_bar(g);   // publish queue entries written by other threads of the group
         PLT_CLK(g0);
         const bool live = t < rows;
-        const int qi = live ? Gs.qi[(qhead + t) & (kQueue - 1)] : 0;
-        float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
+        const int slot = (qhead + t) & (kQueue - 1);
+        Canon k;
+        int qi = 0;
         if (live) {
-            px = __ldg(P.in.ox + qi); py = __ldg(P.in.oy + qi); wx = __ldg(P.in.dx + qi);
-            wy = __ldg(P.in.dy + qi); lam = __ldg(P.in.lambda_nm + qi);
+            const int code = Gs.qi[slot];
+            qi = code & 0x7FFFFFFF;
+            k.flip = code < 0;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) k.x[d] = Gs.qx[d][slot];
+            k.c = Gs.qc[slot]; k.s = Gs.qs[slot];
+        } else {
+#pragma unroll
+            for (int d = 0; d < 4; ++d) k.x[d] = 0.f;
+            k.c = 1.f; k.s = 0.f; k.flip = false;
         }
-        const Canon k = canonicalise(P.mp, px, py, wx, wy, lam);
         store_input(a_row, k.x);
         tmem_st_wait();
 #ifdef PLT_MAP_PROFILE
@@ -644,7 +656,13 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         int before = 0, total = 0;
 #pragma unroll
         for (int w = 0; w < 4; ++w) { const int cw = Gs.wcount[w]; before += w < q ? cw : 0; total += cw; }
-        if (valid) Gs.qi[(qhead + qcount + before + __popc(word & ((1u << lane) - 1u))) & (kQueue - 1)] = (int)i;
+        if (valid) {
+            const int slot = (qhead + qcount + before + __popc(word & ((1u << lane) - 1u))) & (kQueue - 1);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) Gs.qx[d][slot] = k.x[d];
+            Gs.qc[slot] = k.c; Gs.qs[slot] = k.s;
+            Gs.qi[slot] = (int)i | (k.flip ? (int)0x80000000u : 0);
+        }
         qcount += total;
         PLT_CLK(o5);
         if (qcount >= kTile) run_regressor(kTile);
