@@ -1,0 +1,48 @@
+"""Forward flare rendering (Listing 1; Eq. 8).
+
+For every transport path P of the lens (the ghosts of §4.2) and every colour
+channel, the rays of that channel are pushed through P -- by the path's factorised map
+when one is given (eval_map), otherwise by the exact trace -- and the valid exit rays are
+splatted into an int64 film inside the same kernel (plt_*_splat).  The film is the exact
+integer sum of all contributions, so the image does not depend on the order of paths,
+channels or GPUs.  Orchestration only: every step runs in the library's kernels.
+"""
+from __future__ import annotations
+
+from . import FP64, eval_map, trace_rays
+
+
+def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict | None = None,
+                 precision: int = FP64, weight_scale: float = 1.0, direction: int = 0, per_path: dict | None = None,
+                 stream=None, hits=None):
+    """Accumulate the flare image of `path_ids` into `film` (device int64, C*H*W, not cleared;
+    may be None when per_path is given).
+
+    channel_rays: list (one per film channel) of device ray dicts (plt_inputs layout);
+    maps: {path_id: Map} -- paths in it are evaluated by the network, the others traced
+    (precision: PLT_FP64 is binding for ghosts, A22); per_path: optional
+    {path_id: film tensor} receiving each path's own contribution instead of `film`
+    (for per-path comparisons); hits: optional scratch hits dict of >= max rays.
+    Returns the list of (path_id, "map" | "trace") actually used.
+    """
+    import torch
+    from . import alloc_hits
+    used = []
+    dev = channel_rays[0]["ox"].device
+    nmax = max(int(r["ox"].numel()) for r in channel_rays)
+    h = hits if hits is not None else alloc_hits(nmax, device=dev)
+    chan = [torch.full((int(r["ox"].numel()),), c, dtype=torch.uint8, device=dev)
+            for c, r in enumerate(channel_rays)]
+    for pid in path_ids:
+        target = per_path[pid] if per_path is not None else film
+        m = maps.get(int(pid)) if maps else None
+        for c, rays in enumerate(channel_rays):
+            n = int(rays["ox"].numel())
+            spl = {"film_desc": film_desc, "film": target, "channel": chan[c], "weight_scale": weight_scale}
+            if m is not None:
+                eval_map(m, rays, h, n=n, stream=stream, splat=spl)
+            else:
+                trace_rays(lens, int(pid), rays, h, direction=direction, precision=precision, n=n, stream=stream,
+                           splat=spl)
+        used.append((int(pid), "map" if m is not None else "trace"))
+    return used

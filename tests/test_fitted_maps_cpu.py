@@ -54,3 +54,27 @@ def test_committed_map_is_consistent(path):
         ids, _ = lens.enumerate_ghosts(2)
         assert want in ids
     plt.Map(blob, lens=lens)      # host-side validation through the C-ABI (no GPU needed)
+
+
+FLARE = sorted(glob.glob(os.path.join(ROOT, "maps", "flare", "*", "*.pltmap")))
+
+
+def test_flare_maps_belong_to_their_lens():
+    """maps/flare/<config>/<path id>.pltmap (tests/fit_flare_maps.py): every blob is a
+    well-formed network for a two-bounce ghost of that config's lens."""
+    import paper_2605_04017_b200 as plt
+    if not FLARE:
+        pytest.skip("no flare maps committed")
+    by_cfg = {}
+    for path in FLARE:
+        by_cfg.setdefault(os.path.basename(os.path.dirname(path)), []).append(path)
+    for cfg_name, paths in by_cfg.items():
+        cfg = C.CONFIGS[cfg_name]
+        lens = plt.Lens(C.lens_text(cfg_name), **cfg["opts"])
+        ids, _ = lens.enumerate_ghosts(2)
+        ghosts = set(int(i) for i in ids) - {lens.all_t_id()}
+        for path in paths:
+            p = oracle.parse_map_blob(open(path, "rb").read())
+            assert p["path_id"] == int(os.path.basename(path)[:-7]) and p["path_id"] in ghosts
+            assert p["classifier"]["dims"] == list(R.CLASSIFIER_DIMS)
+            assert p["regressor"]["dims"] == list(R.REGRESSOR_DIMS)
