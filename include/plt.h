@@ -256,6 +256,36 @@ PLT_API plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, co
 PLT_API plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir dir, void* buf,
                                        size_t capacity, size_t* size);
 
+/*
+ * Backward camera integrand with a procedural scene (Eq. 9,
+ * P:259-269; the depth-of-field integrator).  For every valid hit of a
+ * PLT_BACKWARD query (exit origin on the plane z = z_hits_mm in the lens frame, direction
+ * towards -z) the ray continues in air to the scene plane z = scene->z_mm (t = (z_s -
+ * z_hits)/w_z > 0 required); the scene radiance is a checkerboard of period `period_mm`:
+ * L = 1 where floor(x/period) + floor(y/period) is even, `contrast` where it is odd.
+ * film[i / spp] += llrint(I * L * weight_scale * 2^32) for ray i (pixel-stratified rays,
+ * e.g. the sensor_grid law), skipping pixels >= `pixels`; IEEE double, exact int64 sum.
+ * film: device, caller-owned, `pixels` int64, NOT cleared.  Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ */
+typedef struct {
+    double z_mm;        /* scene plane (lens frame, object side: below the front vertex) */
+    double period_mm;   /* checker square size, > 0 */
+    double contrast;    /* radiance of the odd squares (even squares: 1) */
+} plt_scene_plane;
+
+PLT_API plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
+                                   int64_t pixels, float weight_scale, int64_t* film, int64_t n, void* cuda_stream);
+
+/*
+ * Free-space propagation to the plane z = z_target_mm (sensor-shift focusing with one
+ * precomputed map): o' = o + ((z_t - z_in)/w_z) w in float32 (round-to-nearest,
+ * one fma per coordinate), w and lambda copied.  in->plane_z_mm is z_in; out's arrays
+ * (device, n each, may alias in's) receive the rays; out->plane_z_mm is not used.
+ * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ */
+PLT_API plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, int64_t n,
+                                      void* cuda_stream);
+
 /* out[i] = film[i] * 2^-32 * scale (float), for channels*height*width pixels. */
 PLT_API plt_status plt_film_resolve(const plt_film_desc* film_desc, const int64_t* film, float* out,
                             double scale, void* cuda_stream);

@@ -15,6 +15,9 @@ O/A = SURVEY.md §8(c) steps/readings, restated in DESIGN.md):
                     (O9-O10), symmetry canonicalisation of §4.1.
 * ``splat``      -- film accumulation of Eq. 8 / Listing 1
                     in int64 fixed point 2^-32 (O11).
+* ``shade_plane``-- backward camera integrand on a checkerboard scene plane (O14,
+                    Eq. 9); ``propagate``: free-space
+                    ray propagation (closed form).
 * ``lens``       -- glass (O1), ABCD (O13), path ids (O2), ghosts (O12).
 
 Pins (tests/test_oracle_*.py) tie every function to something other than
@@ -211,6 +214,30 @@ def splat(film: dict, valid, px, py, dz, I, channel=None, scale: float = 1.0):
                                    p(arrs[0]), p(arrs[1]), p(arrs[2]), p(arrs[3]), p(ch),
                                    np.float32(scale))
     return f, int(dropped)
+
+
+def shade_plane(scene: dict, z_hits: float, valid, px, py, dx, dy, dz, I, spp: int, pixels: int,
+                scale: float = 1.0):
+    """O14 (Eq. 9): backward camera integrand on a
+    checkerboard scene plane -> int64 film of `pixels` (film[i // spp])."""
+    f = np.zeros(int(pixels), np.int64)
+    v = np.ascontiguousarray(valid, dtype=np.uint8)
+    a = [np.ascontiguousarray(x, dtype=np.float32) for x in (px, py, dx, dy, dz, I)]
+    p = _lib.ptr
+    _lib.lib().orc_shade_plane(float(scene["z_mm"]), float(scene["period_mm"]), float(scene["contrast"]),
+                               float(z_hits), int(spp), int(pixels), np.float32(scale), p(f), v.size, p(v),
+                               *[p(x) for x in a])
+    return f
+
+
+def propagate(rays: dict, z_target: float) -> dict:
+    """Free-space propagation to z = z_target in float64 (closed form o + ((z_t - z_0)/w_z) w)."""
+    t = (float(z_target) - float(rays["plane_z"])) / np.asarray(rays["dz"], np.float64)
+    out = {k: np.asarray(rays[k], np.float64).copy() for k in ("dx", "dy", "dz", "lambda_nm")}
+    out["ox"] = np.asarray(rays["ox"], np.float64) + t * out["dx"]
+    out["oy"] = np.asarray(rays["oy"], np.float64) + t * out["dy"]
+    out["plane_z"] = float(z_target)
+    return out
 
 
 def host_threads() -> int:

@@ -325,3 +325,26 @@ int64_t orc_splat(int width, int height, int channels, double W, double H, doubl
     }
     return dropped;
 }
+
+/* ------------------------------------------------------------------------- */
+/* O14 backward camera integrand with a procedural checkerboard scene plane   */
+/* (Eq. 9): exit ray (origin on z = z_hits,   */
+/* direction w) continues to z = z_scene; L = 1 on even squares, contrast on  */
+/* odd ones; film[i / spp] += llrint(I * L * scale * 2^32).                   */
+/* ------------------------------------------------------------------------- */
+void orc_shade_plane(double z_scene, double period, double contrast, double z_hits, int spp, int64_t pixels,
+                     float scale, int64_t* film, int64_t n, const uint8_t* valid, const float* px, const float* py,
+                     const float* dx, const float* dy, const float* dz, const float* I)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        if (!valid[i]) continue;
+        const double t = (z_scene - z_hits) / (double)dz[i];
+        const int64_t pix = i / spp;
+        if (!(t > 0.0) || pix >= pixels) continue;
+        const double x = (double)px[i] + t * (double)dx[i];
+        const double y = (double)py[i] + t * (double)dy[i];
+        const int64_t q = (int64_t)floor(x / period) + (int64_t)floor(y / period);
+        const double L = (q & 1) ? contrast : 1.0;
+        film[pix] += llrint((double)I[i] * L * (double)scale * 4294967296.0);
+    }
+}

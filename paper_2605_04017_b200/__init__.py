@@ -29,7 +29,7 @@ _STATUS = {0: "PLT_OK", 1: "PLT_E_INVALID_ARG", 2: "PLT_E_PARSE", 3: "PLT_E_VALI
 EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "plt_lens_info",
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
-            "plt_trace_jit_cubin")
+            "plt_trace_jit_cubin", "plt_shade_plane", "plt_propagate_rays")
 
 
 class PltError(RuntimeError):
@@ -58,6 +58,10 @@ class FilmDesc(C.Structure):
     _fields_ = [("width_px", C.c_int), ("height_px", C.c_int), ("channels", C.c_int),
                 ("sensor_w_mm", C.c_double), ("sensor_h_mm", C.c_double),
                 ("center_x_mm", C.c_double), ("center_y_mm", C.c_double)]
+
+
+class ScenePlane(C.Structure):
+    _fields_ = [("z_mm", C.c_double), ("period_mm", C.c_double), ("contrast", C.c_double)]
 
 
 class SplatTarget(C.Structure):
@@ -95,9 +99,11 @@ def load():
     L.plt_trace_rays_splat.argtypes = [p, u64, i, i, p, p, p, i64, p]
     L.plt_eval_map_splat.argtypes = [p, p, p, p, p, i64, p]
     L.plt_trace_jit_cubin.argtypes = [p, u64, i, p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.plt_shade_plane.argtypes = [p, d, p, i, i64, C.c_float, p, i64, p]
+    L.plt_propagate_rays.argtypes = [p, p, d, i64, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
-              "plt_eval_map_splat", "plt_trace_jit_cubin"):
+              "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_propagate_rays"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -315,6 +321,27 @@ def splat_sensor(film_d: dict, film, hits: dict, channel=None, weight_scale: flo
                                    float(weight_scale), n,
                                    _ptr(dropped, 1, torch.int64) if dropped is not None else None,
                                    _stream(stream)))
+
+
+def shade_plane(scene: dict, z_hits_mm: float, hits: dict, film, spp: int, pixels: int | None = None,
+                weight_scale: float = 1.0, n: int | None = None, stream=None):
+    """plt_shade_plane: backward camera integrand on a checkerboard scene plane (Eq. 9)."""
+    import torch
+    n = int(hits["px"].numel()) if n is None else int(n)
+    pixels = int(film.numel()) if pixels is None else int(pixels)
+    sc = ScenePlane(float(scene["z_mm"]), float(scene["period_mm"]), float(scene["contrast"]))
+    h = _hits_struct(hits, n)
+    _check(load().plt_shade_plane(C.byref(sc), float(z_hits_mm), C.byref(h), int(spp), pixels, float(weight_scale),
+                                  _ptr(film, pixels, torch.int64), n, _stream(stream)))
+
+
+def propagate_rays(rays: dict, out: dict, z_target_mm: float, n: int | None = None, stream=None):
+    """plt_propagate_rays: free-space propagation to z = z_target_mm (out may alias rays)."""
+    n = _n_of(rays, n)
+    r = _rays_struct(rays, n)
+    o = _rays_struct(dict(out, plane_z=z_target_mm), n)
+    _check(load().plt_propagate_rays(C.byref(r), C.byref(o), float(z_target_mm), n, _stream(stream)))
+    out["plane_z"] = float(z_target_mm)
 
 
 def film_resolve(film_d: dict, film, out, scale: float = 1.0, stream=None):

@@ -256,6 +256,39 @@ plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir d
     PLT_GUARD_END
 }
 
+plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
+                           int64_t pixels, float weight_scale, int64_t* film, int64_t n, void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (!scene || !hits || !film) return set_err(PLT_E_INVALID_ARG, "null scene/hits/film");
+    if (!(scene->period_mm > 0) || !std::isfinite(scene->z_mm) || !std::isfinite(scene->contrast) ||
+        !std::isfinite(z_hits_mm))
+        return set_err(PLT_E_INVALID_ARG, "bad scene plane");
+    if (spp <= 0 || pixels <= 0 || n < 0) return set_err(PLT_E_INVALID_ARG, "spp, pixels must be > 0 and n >= 0");
+    if (n == 0) return PLT_OK;
+    if (!hits->mask_bits || !hits->px || !hits->py || !hits->dx || !hits->dy || !hits->dz || !hits->throughput)
+        return set_err(PLT_E_INVALID_ARG, "null hit arrays");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    const plt::ScenePlane sc{scene->z_mm, scene->period_mm, scene->contrast};
+    return cuda_status(plt::launch_shade_plane(sc, z_hits_mm, *hits, spp, pixels, weight_scale, film, n, cuda_stream),
+                       "shade_plane");
+    PLT_GUARD_END
+}
+
+plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, int64_t n,
+                              void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
+    if (n == 0) return PLT_OK;
+    if (!rays_ok(in) || !out || !out->ox || !out->oy || !out->dx || !out->dy || !out->dz || !out->lambda_nm ||
+        !std::isfinite(z_target_mm))
+        return set_err(PLT_E_INVALID_ARG, "null ray pointer or non-finite plane");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    return cuda_status(plt::launch_propagate(*in, *out, (float)z_target_mm, n, cuda_stream), "propagate_rays");
+    PLT_GUARD_END
+}
+
 plt_status plt_film_resolve(const plt_film_desc* fd, const int64_t* film, float* out, double scale, void* cuda_stream) {
     PLT_GUARD_BEGIN
     if (!fd || !film || !out) return set_err(PLT_E_INVALID_ARG, "null film/out");

@@ -9,7 +9,7 @@ channels or GPUs.  Orchestration only: every step runs in the library's kernels.
 """
 from __future__ import annotations
 
-from . import FP64, eval_map, trace_rays
+from . import BACKWARD, FP32, FP64, eval_map, propagate_rays, shade_plane, trace_rays
 
 
 def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict | None = None,
@@ -46,3 +46,30 @@ def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict
                            splat=spl)
         used.append((int(pid), "map" if m is not None else "trace"))
     return used
+
+
+def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, m=None, map_plane_z: float | None = None,
+               weight_scale: float = 1.0, hits=None, scratch_rays=None, stream=None):
+    """Backward depth-of-field image (the camera integrator of
+    P:422-427, Eq. 9): pixel-stratified sensor rays (e.g. the sensor_grid law, ray i in
+    pixel i // spp) go through the lens -- by the exact all-T trace, or by the map `m`
+    after free-space propagation to the map's input plane `map_plane_z` (focusing by a
+    sensor shift needs no retraining) -- and their exit rays (on z = z_exit_mm,
+    the lens's backward exit plane) are shaded on the checkerboard scene plane into `film`
+    (device int64, one entry per pixel, not cleared).
+    """
+    from . import alloc_hits
+    import torch
+    n = int(rays["ox"].numel())
+    h = hits if hits is not None else alloc_hits(n, device=rays["ox"].device)
+    if m is None:
+        trace_rays(lens, lens.all_t_id(), rays, h, direction=BACKWARD, precision=FP32, stream=stream)
+    else:
+        src = rays
+        if map_plane_z is not None and float(map_plane_z) != float(rays["plane_z"]):
+            dst = scratch_rays if scratch_rays is not None else {k: torch.empty_like(rays[k]) for k in
+                                                                 ("ox", "oy", "dx", "dy", "dz", "lambda_nm")}
+            propagate_rays(rays, dst, map_plane_z, stream=stream)
+            src = dst
+        eval_map(m, src, h, stream=stream)
+    shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale, n=n, stream=stream)

@@ -58,6 +58,18 @@ CONFIGS = {
            "map_norm": {"in_lo": (0.0, -0.8, 0.0, 400.0), "in_hi": (14.5, 0.8, 0.8, 700.0),
                         "out_mid": (0.0, 0.0, 0.0, 0.0, -0.8, 0.5),
                         "out_half": (30.0, 30.0, 0.8, 0.8, 0.2, 0.5)}},
+    # C3 as a depth-of-field camera: pixel-stratified rays of a
+    # 192 x 128 image over the 24 x 16 mm sensor, a checkerboard scene plane 1 m in front of
+    # the lens (object side, lens frame), sensor shifts for the focus sweep
+    "C3_DOF": {"lens": "wide24", "direction": BACKWARD,
+               "opts": lens_opts(sensor_z_mm=WIDE24_SENSOR_Z, sensor_w_mm=24.0, sensor_h_mm=16.0,
+                                 backward_exit_z_mm=-5.0),
+               "seed": 33, "width_px": 192, "height_px": 128, "spp": 64,
+               "scene": {"z_mm": -1000.0, "period_mm": 50.0, "contrast": 0.1},
+               "sensor_shifts_mm": (-1.0, 0.0, 0.6, 1.5),
+               "law": {"kind": "sensor_grid", "plane_z": WIDE24_SENSOR_Z, "sensor_w": 24.0, "sensor_h": 16.0,
+                       "width_px": 192, "height_px": 128, "spp": 64, "pupil_z": WIDE24_REAR_VERTEX_Z,
+                       "pupil_r": 9.8055, "lam": (400.0, 700.0)}},
     # C4 flare: 22 mm @ 15 deg and 59 mm @ 10 deg, 2^20 rays per ghost per RGB channel
     "C4_22": {"lens": "wide22", "direction": FORWARD,
               "opts": lens_opts(sensor_w_mm=24.0, sensor_h_mm=16.0), "seed": 4,
@@ -81,6 +93,16 @@ CONFIGS = {
            "law": {"kind": "disc_cap", "plane_z": -5.0, "disc_r": 1.05 * 12.6, "cap_deg": 25.0,
                    "lam": (400.0, 700.0)}},
 }
+
+
+def dof_law(shift_mm: float = 0.0, spp: int | None = None) -> dict:
+    """C3_DOF rays with the sensor moved by shift_mm along z (away from the lens for > 0)."""
+    cfg = CONFIGS["C3_DOF"]
+    law = dict(cfg["law"])
+    law["plane_z"] = law["plane_z"] + shift_mm
+    if spp is not None:
+        law["spp"] = spp
+    return law
 
 
 def lens_text(cfg_name: str) -> str:

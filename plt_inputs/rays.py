@@ -59,6 +59,9 @@ def gen_chunk(law: dict, seed: int, c: int, count: int = CHUNK) -> dict:
         rectangle ``sensor_w`` x ``sensor_h`` at ``plane_z``; direction towards
         a point uniform on the disc of radius ``pupil_r`` at ``pupil_z``
         (normalised), pointing to -z.
+      kind="sensor_grid": as sensor_pupil, but stratified by pixel: global ray i
+        starts in pixel i // ``spp`` of a ``width_px`` x ``height_px`` sensor grid
+        (row-major, row 0 at +y).
     """
     rng = _chunk_rng(seed, c)
     kind = law["kind"]
@@ -75,6 +78,21 @@ def gen_chunk(law: dict, seed: int, c: int, count: int = CHUNK) -> dict:
     elif kind == "sensor_pupil":
         ox = (rng.random(count) - 0.5) * law["sensor_w"]
         oy = (rng.random(count) - 0.5) * law["sensor_h"]
+        px, py = _uniform_disc(rng, count, law["pupil_r"])
+        vz = law["pupil_z"] - law["plane_z"]
+        vx, vy = px - ox, py - oy
+        inv = 1.0 / np.sqrt(vx * vx + vy * vy + vz * vz)
+        dx, dy, dz = vx * inv, vy * inv, np.full(count, vz) * inv
+    elif kind == "sensor_grid":
+        # pixel-stratified backward camera rays: global ray i belongs to pixel i // spp
+        # (row-major, row 0 at +y), origin uniform within that pixel, direction towards a
+        # point uniform on the rear pupil disc (as sensor_pupil)
+        W, H, spp = law["width_px"], law["height_px"], law["spp"]
+        gi = c * CHUNK + np.arange(count, dtype=np.int64)
+        pix = gi // spp
+        ix, iy = pix % W, pix // W
+        ox = -0.5 * law["sensor_w"] + (ix + rng.random(count)) * (law["sensor_w"] / W)
+        oy = 0.5 * law["sensor_h"] - (iy + rng.random(count)) * (law["sensor_h"] / H)
         px, py = _uniform_disc(rng, count, law["pupil_r"])
         vz = law["pupil_z"] - law["plane_z"]
         vx, vy = px - ox, py - oy

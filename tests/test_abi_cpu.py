@@ -166,3 +166,26 @@ def test_trace_jit_compiles_without_gpu(plt, name, path, direction):
     L = plt.Lens(CF.lens_text(name), **cfg["opts"])
     cubin = L.trace_jit_cubin(path or L.all_t_id(), direction)
     assert cubin[:4] == b"\x7fELF" and b"plt_trace_jit" in cubin
+
+
+def test_camera_entry_points_validate_then_fail_loudly(plt):
+    """plt_shade_plane / plt_propagate_rays: bad arguments are PLT_E_INVALID_ARG before the
+    device is touched; valid calls need the GPU (PLT_E_CUDA)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = plt.load()
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    rays = plt.Rays(*fake[:6], 52.0)
+    hits = plt.Hits(*fake[:7], None)
+    good = plt.ScenePlane(-1000.0, 50.0, 0.1)
+    bad = plt.ScenePlane(-1000.0, 0.0, 0.1)
+    film = C.c_void_p(1 << 20)
+    assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 4, 100, 1.0, film, 10, None) == 6
+    assert lib.plt_shade_plane(C.byref(bad), -5.0, C.byref(hits), 4, 100, 1.0, film, 10, None) == 1
+    assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 0, 100, 1.0, film, 10, None) == 1
+    assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 4, 100, 1.0, None, 10, None) == 1
+    assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 4, 100, 1.0, film, 0, None) == 0
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, 10, None) == 6
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), float("nan"), 10, None) == 1
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, -1, None) == 1

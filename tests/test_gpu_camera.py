@@ -1,0 +1,94 @@
+"""GPU parity of the backward camera integrand (plt_shade_plane, O14) and free-space
+propagation (plt_propagate_rays) against the oracle, and the depth-of-field camera of
+SURVEY §8(f) NEXT-3: map image vs exact-trace image on the same rays, and the
+sensor-shift focus sweep with one precomputed map."""
+import numpy as np
+import pytest
+
+import oracle
+from plt_inputs import configs as C
+from plt_inputs import rays as R
+
+from gpu_helpers import unpack_mask
+
+pytestmark = pytest.mark.gpu
+
+SCENE = C.CONFIGS["C3_DOF"]["scene"]
+
+
+@pytest.mark.parametrize("spp", [1, 7, 64])
+def test_shade_plane_bit_exact_on_trace_hits(gpu_lib, spp):
+    import torch
+    plt = gpu_lib
+    cfg = C.CONFIGS["C3_DOF"]
+    lens = plt.Lens(C.lens_text("C3_DOF"), **cfg["opts"])
+    law = C.dof_law(0.0, spp)
+    n = cfg["width_px"] * cfg["height_px"] * spp // 4 + 13          # ragged: last pixel partial
+    d = plt.rays_to_device(R.gen_rays(law, 5, 0, n))
+    h = plt.alloc_hits(n)
+    plt.trace_rays(lens, lens.all_t_id(), d, h, direction=plt.BACKWARD)
+    pixels = (n + spp - 1) // spp - 2                                 # some rays beyond the film
+    film = torch.zeros(pixels, dtype=torch.int64, device="cuda")
+    plt.shade_plane(SCENE, cfg["opts"]["backward_exit_z_mm"], h, film, spp, pixels=pixels, weight_scale=0.5)
+    torch.cuda.synchronize()
+    hh = {k: h[k].cpu().numpy() for k in plt.HIT_KEYS}
+    valid = unpack_mask(h["mask_bits"].cpu().numpy(), n)
+    ref = oracle.shade_plane(SCENE, cfg["opts"]["backward_exit_z_mm"], valid, hh["px"], hh["py"], hh["dx"], hh["dy"],
+                             hh["dz"], hh["throughput"], spp=spp, pixels=pixels, scale=0.5)
+    assert valid.mean() > 0.02
+    assert np.array_equal(film.cpu().numpy(), ref)
+
+
+def test_propagate_matches_closed_form(gpu_lib):
+    import torch
+    plt = gpu_lib
+    law = C.dof_law(1.5, 16)
+    rays = R.gen_rays(law, 9, 0, 100_003)
+    d = plt.rays_to_device(rays)
+    out = {k: torch.empty_like(d[k]) for k in plt.RAY_KEYS}
+    z0 = C.CONFIGS["C3"]["law"]["plane_z"]
+    plt.propagate_rays(d, out, z0)
+    torch.cuda.synchronize()
+    ref = oracle.propagate(rays, z0)
+    for k in ("ox", "oy"):
+        assert np.max(np.abs(out[k].cpu().numpy() - ref[k])) <= 2e-5
+    for k in ("dx", "dy", "dz", "lambda_nm"):
+        assert np.array_equal(out[k].cpu().numpy(), rays[k])
+    plt.propagate_rays(d, d, z0)                                       # in place (aliasing allowed)
+    torch.cuda.synchronize()
+    assert torch.equal(d["ox"], out["ox"]) and torch.equal(d["oy"], out["oy"])
+
+
+def test_dof_map_vs_trace_and_focus_sweep(gpu_lib):
+    import torch
+    from paper_2605_04017_b200.render import render_dof
+    plt = gpu_lib
+    cfg = C.CONFIGS["C3_DOF"]
+    lens = plt.Lens(C.lens_text("C3_DOF"), **cfg["opts"])
+    m = plt.Map(C.fitted_map_blob("C3"), lens=lens)
+    spp = 256
+    W, H = cfg["width_px"], cfg["height_px"]
+
+    def sharp(img):
+        return float(np.abs(np.diff(img, axis=1)).mean() + np.abs(np.diff(img, axis=0)).mean()) / img.mean()
+
+    res = {}
+    for shift in (-1.0, 0.6, 1.5):
+        d = plt.rays_to_device(R.gen_rays(C.dof_law(shift, spp), cfg["seed"], 0, W * H * spp))
+        imgs = {}
+        for key, mm in (("trace", None), ("map", m)):
+            film = torch.zeros(W * H, dtype=torch.int64, device="cuda")
+            render_dof(lens, d, SCENE, film, spp, cfg["opts"]["backward_exit_z_mm"], m=mm,
+                       map_plane_z=C.CONFIGS["C3"]["law"]["plane_z"], weight_scale=1.0 / spp)
+            torch.cuda.synchronize()
+            imgs[key] = film.double().cpu().numpy().reshape(H, W)
+        t, mp = imgs["trace"], imgs["map"]
+        lit = t > 0
+        res[shift] = {"mape": float(np.mean(np.abs(mp[lit] - t[lit]) / t[lit])), "energy": float(mp.sum() / t.sum()),
+                      "sharp_t": sharp(t), "sharp_m": sharp(mp)}
+    print(res)
+    for r in res.values():
+        assert r["mape"] <= 0.08 and abs(r["energy"] - 1) <= 0.04
+        assert abs(r["sharp_m"] / r["sharp_t"] - 1) <= 0.03
+    for key in ("sharp_t", "sharp_m"):      # the object plane focuses ~0.6 mm behind the infinity focus
+        assert res[0.6][key] > res[-1.0][key] and res[0.6][key] > res[1.5][key]
