@@ -125,9 +125,12 @@ PLT_API plt_status plt_lens_info(const plt_lens* lens, double lambda_nm, int* n_
  *
  * plt_enumerate_ghosts lists the all-T path followed by every two-bounce ghost
  * ("contributions from higher-order paths ... are negligible"), ascending
- * by id.  max_bounces: 0 (all-T only) or 2.  min_throughput > 0 drops ghosts whose
- * normal-incidence throughput R_i R_j prod T at lambda_ref is below it.
- * ij_pairs (nullable) receives (i, j) per id ((0,0) for all-T).
+ * by id.  max_bounces: 0 (all-T only), 2, or 4: adds the four-bounce paths that
+ * reflect at i, then j < i, then k > j, then l < k (ids with
+ * K > 63 interactions are skipped).  min_throughput > 0 drops paths whose
+ * normal-incidence throughput (product of R at the reflections and T elsewhere) at
+ * lambda_ref is below it.  ij_pairs (nullable) receives the first reflection pair
+ * (i, j) per id ((0,0) for all-T).
  * Two-call pattern: with ids == NULL or capacity < count, *count is set and
  * PLT_E_CAPACITY is returned.
  */

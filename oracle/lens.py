@@ -230,20 +230,45 @@ def _walk_normal_incidence(lens: OracleLens, path_id: int, lam_nm: float):
     return I
 
 
+def ghost4_id(m: int, i: int, j: int, k: int, l: int) -> int:
+    """Four-bounce path reflecting at optical surfaces i, j, k, l in that order
+    (1 <= j < i <= m, j < k <= m, 1 <= l < k): interactions forward to i, back to j,
+    forward to k, back to l, forward out."""
+    K = m + 2 * (i - j) + 2 * (k - l)
+    r1 = i - 1
+    r2 = r1 + (i - j)
+    r3 = r2 + (k - j)
+    r4 = r3 + (k - l)
+    return (1 << K) | (1 << r1) | (1 << r2) | (1 << r3) | (1 << r4)
+
+
 def enumerate_ghosts(lens: OracleLens, max_bounces: int = 2, min_throughput: float = 0.0,
                      lam_nm: float = 587.5618):
     """O12: all (i, j), 1 <= j < i <= m, ascending by id; optional normal-incidence prune.
-    max_bounces = 0 returns the all-T path only; 2 returns the all-T path plus ghosts."""
+    max_bounces = 0 returns the all-T path only; 2 returns the all-T path plus ghosts;
+    4 adds the four-bounce paths (i, j, k, l) of ghost4_id, their pair given as (i, j)."""
     m = lens.n_optical
     items = [(all_t_id(m), (0, 0))]
+
+    def keep(pid):
+        if min_throughput <= 0.0:
+            return True
+        thr = _walk_normal_incidence(lens, pid, lam_nm)
+        return thr is not None and thr >= min_throughput
+
     if max_bounces >= 2:
         for i in range(2, m + 1):
             for j in range(1, i):
                 pid = ghost_id(m, i, j)
-                if min_throughput > 0.0:
-                    thr = _walk_normal_incidence(lens, pid, lam_nm)
-                    if thr is None or thr < min_throughput:
-                        continue
-                items.append((pid, (i, j)))
+                if keep(pid):
+                    items.append((pid, (i, j)))
+    if max_bounces >= 4:
+        for j in range(1, m):
+            for i in range(j + 1, m + 1):
+                for k in range(j + 1, m + 1):
+                    for l in range(1, k):
+                        pid = ghost4_id(m, i, j, k, l)
+                        if keep(pid):
+                            items.append((pid, (i, j)))
     items.sort()
     return [p for p, _ in items], [ij for _, ij in items]

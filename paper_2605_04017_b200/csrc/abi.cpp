@@ -97,8 +97,8 @@ plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, double mi
                                 int32_t* ij_pairs, int capacity, int* count) {
     PLT_GUARD_BEGIN
     if (!lens || !count) return set_err(PLT_E_INVALID_ARG, "lens and count must be non-null");
-    if (max_bounces != 0 && max_bounces != 2)
-        return set_err(PLT_E_UNSUPPORTED, "max_bounces must be 0 or 2 (P:339: higher orders negligible)");
+    if (max_bounces != 0 && max_bounces != 2 && max_bounces != 4)
+        return set_err(PLT_E_UNSUPPORTED, "max_bounces must be 0, 2 or 4 (P:339: higher orders negligible)");
     auto v = plt::enumerate_ghosts(*lens, max_bounces, min_throughput);
     *count = (int)v.size();
     if (!ids || capacity < (int)v.size())

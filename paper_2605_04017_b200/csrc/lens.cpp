@@ -384,7 +384,7 @@ std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, 
     int s = 0, d = +1, k = 0, ns = 0;
     const int S = (int)fr.size();
     while (s >= 0 && s < S) {
-        if (ns >= kMaxSteps) fail(PLT_E_INVALID_ARG, "path needs more than 40 surface steps");
+        if (ns >= kMaxSteps) fail(PLT_E_INVALID_ARG, "path needs more than " + std::to_string(kMaxSteps) + " surface steps");
         const Surface& sf = fr[s];
         if (sf.stop) {
             fill_step(&cp->pf.st[ns], sf, kStop, 0, d, sf.after);
@@ -473,16 +473,29 @@ std::vector<std::pair<uint64_t, std::pair<int, int>>> enumerate_ghosts(const plt
     const int m = L.n_optical;
     std::vector<std::pair<uint64_t, std::pair<int, int>>> out;
     out.push_back({1ull << m, {0, 0}});
+    auto keep = [&](uint64_t id) {
+        return !(min_throughput > 0.0 && normal_incidence_throughput(L, id, L.opts.lambda_ref_nm) < min_throughput);
+    };
     if (max_bounces >= 2) {
         for (int i = 2; i <= m; ++i)
             for (int j = 1; j < i; ++j) {
                 const int K = m + 2 * (i - j);
                 if (K > 63) continue;
                 uint64_t id = (1ull << K) + (1ull << (i - 1)) + (1ull << (2 * i - j - 1));
-                if (min_throughput > 0.0 && normal_incidence_throughput(L, id, L.opts.lambda_ref_nm) < min_throughput)
-                    continue;
-                out.push_back({id, {i, j}});
+                if (keep(id)) out.push_back({id, {i, j}});
             }
+    }
+    if (max_bounces >= 4) {   // reflect at i, back to j, forward to k, back to l (NEXT-4)
+        for (int j = 1; j < m; ++j)
+            for (int i = j + 1; i <= m; ++i)
+                for (int k = j + 1; k <= m; ++k)
+                    for (int l = 1; l < k; ++l) {
+                        const int K = m + 2 * (i - j) + 2 * (k - l);
+                        if (K > 63) continue;
+                        const int r1 = i - 1, r2 = r1 + (i - j), r3 = r2 + (k - j), r4 = r3 + (k - l);
+                        const uint64_t id = (1ull << K) | (1ull << r1) | (1ull << r2) | (1ull << r3) | (1ull << r4);
+                        if (keep(id)) out.push_back({id, {i, j}});
+                    }
     }
     std::sort(out.begin(), out.end());
     return out;

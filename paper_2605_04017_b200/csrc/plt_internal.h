@@ -16,7 +16,7 @@ namespace plt {
 // it travels).  The device executes the sequence; the program travels as a
 // __grid_constant__ kernel parameter (read through the constant bank).
 // ---------------------------------------------------------------------------
-constexpr int kMaxSteps = 40;   // two-bounce ghosts of a 12-surface lens + 3 stop crossings = 37
+constexpr int kMaxSteps = 72;   // four-bounce paths of a 13-surface lens: <= 61 interactions + stop crossings
 
 enum StepKind : int { kSphere = 0, kPlane = 1, kStop = 2 };
 enum GlassForm : int { kCauchyForm = 0, kSellmeier = 1 };

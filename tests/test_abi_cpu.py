@@ -55,7 +55,7 @@ def test_lens_info_matches_oracle_abcd(plt, name):
 def test_ghost_enumeration_matches_oracle(plt, name):
     L = plt.Lens(LENSES[name])
     O = oracle.load_lens(LENSES[name])
-    for mb, thr in ((0, 0.0), (2, 0.0), (2, 1e-5), (2, 1e-3)):
+    for mb, thr in ((0, 0.0), (2, 0.0), (2, 1e-5), (2, 1e-3), (4, 0.0), (4, 1e-6)):
         ids, ij = L.enumerate_ghosts(mb, thr)
         oids, oij = oracle.enumerate_ghosts(O, mb, thr)
         assert ids == oids and ij == [tuple(x) for x in oij]

@@ -121,6 +121,27 @@ def test_c4_ghosts_fp64_parity(gpu_lib, cfg_name):
     assert nval > 100
 
 
+@pytest.mark.parametrize("cfg_name", ["C4_22", "C4_59"])
+def test_four_bounce_paths_fp64_parity(gpu_lib, cfg_name):
+    """Four-bounce paths (up to 60+ surface steps): the brightest ones
+    by normal-incidence throughput, float64 trace vs the oracle, flare rays."""
+    plt = gpu_lib
+    cfg = C.CONFIGS[cfg_name]
+    gl, ol = _lenses(plt, cfg["lens"], cfg["opts"])
+    ids4, _ = gl.enumerate_ghosts(4, 1e-9)
+    ids2, _ = gl.enumerate_ghosts(2)
+    four = sorted(set(ids4) - set(ids2))
+    thr = {p: oracle.lens._walk_normal_incidence(ol, p, 587.5618) for p in four}
+    pick = sorted(four, key=lambda p: -thr[p])[:5] + [max(four)]     # brightest + the longest path
+    rays = C.flare_rays(cfg_name, 1, 0, 1 << 15)
+    nval = 0
+    for pid in pick:
+        o = oracle.trace(ol, int(pid), 0, rays, threads=oracle.host_threads())
+        g64 = gpu_trace(plt, gl, int(pid), rays, precision=1)
+        nval += compare_trace(g64, o, tol_p=4e-6, tol_w=2e-7, tol_i=2e-7)["n_both"]
+    assert nval > 20
+
+
 def test_invalid_path_id_and_empty(gpu_lib):
     plt = gpu_lib
     gl = plt.Lens(LENSES["dgauss50"])

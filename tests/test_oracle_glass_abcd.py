@@ -1,4 +1,5 @@
 """Pins for oracle O1 (glass), O13 (ABCD) and O2/O12 (path ids, ghosts) -- CPU only."""
+import itertools
 import json
 import math
 import os
@@ -147,3 +148,27 @@ def test_ghost_prune_is_monotone():
     slab = oracle.load_lens(_slab_text(2), {"sensor_z_mm": 50.0})
     thr = oracle.lens._walk_normal_incidence(slab, ghost_id(2, 2, 1), LD)
     assert abs(thr - 0.96 * 0.04 * 0.04 * 0.96) < 1e-15
+
+
+def test_four_bounce_enumeration_is_complete_and_consistent():
+    """O12 with max_bounces = 4: the four-bounce ids are exactly the
+    bit strings with four R whose surface walk enters at the front and leaves at the back
+    (brute force over every such string), and their count follows the closed form
+    sum_j (m - j) * sum_{k > j} (k - 1)."""
+    L = oracle.load_lens(_slab_text(4), {"sensor_z_mm": 50.0})
+    m = 4
+    brute = set()
+    for K in range(m, m + 4 * m):
+        for bits in itertools.combinations(range(K), 4):
+            pid = (1 << K) | sum(1 << b for b in bits)
+            if oracle.lens._walk_normal_incidence(L, pid, LD) is not None:
+                brute.add(pid)
+    ids4, _ = oracle.enumerate_ghosts(L, 4)
+    ids2, _ = oracle.enumerate_ghosts(L, 2)
+    four = set(ids4) - set(ids2)
+    assert four == brute
+    assert len(four) == sum((m - j) * sum(k - 1 for k in range(j + 1, m + 1)) for j in range(1, m))
+    # normal-incidence throughput of a four-bounce path through a 2-surface slab: T R R R R T
+    slab = oracle.load_lens(_slab_text(2), {"sensor_z_mm": 50.0})
+    pid = oracle.lens.ghost4_id(2, 2, 1, 2, 1)
+    assert abs(oracle.lens._walk_normal_incidence(slab, pid, LD) - 0.96 * 0.04 ** 4 * 0.96) < 1e-18
