@@ -26,5 +26,13 @@ for n in (1, 37, 4096 + 37):
     plt.splat_sensor(fd, film, h, weight_scale=1.0)
     out = torch.empty(64 * 48, device="cuda")
     plt.film_resolve(fd, film, out)
+    # fused query + splat, camera shading and propagation
+    spl = {"film_desc": fd, "film": film, "weight_scale": 1.0}
+    plt.trace_rays(lens, pid, rays, h, splat=spl)
+    plt.trace_rays(lens, pid, rays, h, precision=plt.FP64, splat=spl)
+    plt.eval_map(m, rays, h, splat=spl)
+    plt.shade_plane({"z_mm": -1000.0, "period_mm": 50.0, "contrast": 0.1}, -5.0, h, film, 3)
+    dst = {k: torch.empty_like(rays[k]) for k in plt.RAY_KEYS}
+    plt.propagate_rays(rays, dst, -4.0)
 torch.cuda.synchronize()
 print("sanitize smoke done")
