@@ -29,6 +29,11 @@ class Surface:
     is_stop: bool
     glass_before: tuple = AIR
     glass_after: tuple = AIR
+    # even asphere: sag(rho) = c rho^2 / (1 + sqrt(1 - (1 + k) c^2 rho^2))
+    #   + A4 rho^4 + A6 rho^6 + A8 rho^8 + A10 rho^10, c = 1/R (0 for R = 0)
+    asph: bool = False
+    k: float = 0.0
+    A: tuple = (0.0, 0.0, 0.0, 0.0)
 
 
 @dataclass
@@ -75,15 +80,28 @@ def _glass_token(tok: str, vd: str | None = None):
     return (GLASS_CONST, (nd, 0, 0, 0, 0, 0))
 
 
+def _asph_token(tok: str):
+    """'asph:k,A4,A6,A8,A10' (missing trailing coefficients are 0)."""
+    v = [float(x) for x in tok.split(":", 1)[1].split(",")]
+    v = (v + [0.0] * 5)[:5]
+    return v[0], tuple(v[1:])
+
+
 def parse_lens(text: str, opts: dict | None = None) -> OracleLens:
-    """Parse the repo's .lens table (or a JSON document with a 'surfaces' list)."""
+    """Parse the repo's .lens table (or a JSON document with a 'surfaces' list).
+    Table rows: radius thickness glass aperture_diameter [V_d] [asph:k,A4,A6,A8,A10];
+    JSON surfaces may carry "conic" and "aspheric": [A4, A6, A8, A10]."""
     rows, name = [], "lens"
     if text.lstrip().startswith("{"):
         doc = json.loads(text)
         name = doc.get("name", name)
         for s in doc["surfaces"]:
+            asph = None
+            if "conic" in s or "aspheric" in s:
+                A = tuple((list(map(float, s.get("aspheric", []))) + [0.0] * 4)[:4])
+                asph = (float(s.get("conic", 0.0)), A)
             rows.append((float(s["radius_mm"]), float(s["thickness_mm"]),
-                         _glass_token(str(s["glass"])), 2.0 * float(s["semi_aperture_mm"])))
+                         _glass_token(str(s["glass"])), 2.0 * float(s["semi_aperture_mm"]), asph))
     else:
         for line in text.splitlines():
             body = line.split("#", 1)[0].strip()
@@ -93,14 +111,20 @@ def parse_lens(text: str, opts: dict | None = None) -> OracleLens:
             if tok[0] == "name":
                 name = tok[1]
                 continue
+            asph = None
+            if tok[-1].lower().startswith("asph:"):
+                asph = _asph_token(tok[-1])
+                tok = tok[:-1]
             vd = tok[4] if len(tok) > 4 else None
-            rows.append((float(tok[0]), float(tok[1]), _glass_token(tok[2], vd), float(tok[3])))
+            rows.append((float(tok[0]), float(tok[1]), _glass_token(tok[2], vd), float(tok[3]), asph))
     surfaces, z, prev = [], 0.0, AIR
-    for (r, t, g, d) in rows:
+    for (r, t, g, d, asph) in rows:
         stop = g is None
         after = prev if stop else g
-        surfaces.append(Surface(z=z, R=0.0 if stop else r, a=0.5 * d, is_stop=stop,
-                                glass_before=prev, glass_after=after))
+        sf = Surface(z=z, R=0.0 if stop else r, a=0.5 * d, is_stop=stop, glass_before=prev, glass_after=after)
+        if asph is not None and not stop:
+            sf.asph, sf.k, sf.A = True, asph[0], asph[1]
+        surfaces.append(sf)
         prev = after
         z += t
     lens = OracleLens(name=name, surfaces=surfaces, opts=dict(opts or {}))
@@ -114,23 +138,28 @@ def glass_index(g, lam_nm: float) -> float:
 
 
 def mirrored(lens: OracleLens) -> list:
-    """C0 backward mode: z' = z_S - z, R' = -R, order reversed, before/after swapped."""
+    """C0 backward mode: z' = z_S - z, R' = -R (and A' = -A: the mirrored sag is -sag),
+    order reversed, before/after swapped."""
     zS = lens.surfaces[-1].z
     out = []
     for s in reversed(lens.surfaces):
         out.append(Surface(z=zS - s.z, R=-s.R if s.R != 0.0 else 0.0, a=s.a, is_stop=s.is_stop,
-                           glass_before=s.glass_after, glass_after=s.glass_before))
+                           glass_before=s.glass_after, glass_after=s.glass_before,
+                           asph=s.asph, k=s.k, A=tuple(-x for x in s.A)))   # sag' = -sag
     return out
 
 
 def surface_array(surfs: list) -> np.ndarray:
-    a = np.zeros((len(surfs), 18), dtype=np.float64)
+    a = np.zeros((len(surfs), 24), dtype=np.float64)
     for i, s in enumerate(surfs):
         a[i, 0], a[i, 1], a[i, 2], a[i, 3] = s.z, s.R, s.a, 1.0 if s.is_stop else 0.0
         a[i, 4] = s.glass_before[0]
         a[i, 5:11] = s.glass_before[1]
         a[i, 11] = s.glass_after[0]
         a[i, 12:18] = s.glass_after[1]
+        a[i, 18] = 1.0 if s.asph else 0.0
+        a[i, 19] = s.k
+        a[i, 20:24] = s.A
     return a
 
 

@@ -54,7 +54,8 @@ double orc_glass_index(int model, const double* c, double lambda_nm)
 /*  [0] z vertex  [1] R signed (0 = plane)  [2] a clear semi-aperture          */
 /*  [3] is_stop   [4] glass-before model  [5..10] coeffs                       */
 /*  [11] glass-after model  [12..17] coeffs                                    */
-#define ORC_STRIDE 18
+/*  [18] is_asph  [19] conic k  [20..23] A4, A6, A8, A10 (even asphere)        */
+#define ORC_STRIDE 24
 
 /* Lens-level parameters: [0] housing radius (0 = none) [1] z of output plane  */
 /* [2] rect W (0 = none) [3] rect H [4] rect cx [5] rect cy                    */
@@ -64,6 +65,23 @@ double orc_glass_index(int model, const double* c, double lambda_nm)
 static inline double dot3(const double* a, const double* b)
 {
     return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+/* Even asphere: sag(rho) = c rho^2 / (1 + sqrt(q))          */
+/* + A4 rho^4 + A6 rho^6 + A8 rho^8 + A10 rho^10 with q = 1 - (1 + k) c^2 rho^2, and      */
+/* g = (d sag / d rho) / rho = c / sqrt(q) + 4 A4 rho^2 + 6 A6 rho^4 + 8 A8 rho^6 + 10 A10 rho^8. */
+/* Returns 0 outside the conic's domain (q < 0).                                          */
+static int asph_sag(const double* f, double c, double r2, double* sag, double* g, double* q_out)
+{
+    const double k = f[19], A4 = f[20], A6 = f[21], A8 = f[22], A10 = f[23];
+    const double q = 1.0 - (1.0 + k) * c * c * r2;
+    *q_out = q;
+    if (q < 0.0) return 0;
+    const double sq = sqrt(q);
+    *sag = c * r2 / (1.0 + sq) + A4 * r2 * r2 + A6 * r2 * r2 * r2 + A8 * r2 * r2 * r2 * r2 +
+           A10 * r2 * r2 * r2 * r2 * r2;
+    *g = c / sq + 4.0 * A4 * r2 + 6.0 * A6 * r2 * r2 + 8.0 * A8 * r2 * r2 * r2 + 10.0 * A10 * r2 * r2 * r2 * r2;
+    return 1;
 }
 
 /*
@@ -98,8 +116,34 @@ static int trace_one(const double* S, int n_surf, const double* L, uint64_t path
 
         /* O5 intersection, vertex-local */
         const double lx = o[0], ly = o[1], lz = o[2] - zs;
-        double t;
-        if (R == 0.0 || is_stop) {
+        const int asph = !is_stop && f[18] != 0.0;
+        double t, ga = 0.0;   /* asphere: g at the hit */
+        if (asph) {
+            /* Newton on F(t) = (lz + t wz) - sag(rho(t)), F'(t) = wz - g (x wx + y wy), from the
+               tangent plane z = vertex (the plain algorithm; no base-sphere shortcut). */
+            const double c = (R == 0.0) ? 0.0 : 1.0 / R;
+            t = -lz / w[2];
+            int ok = 0;
+            double Fp = 0.0;
+            for (int it = 0; it < 100; ++it) {
+                const double x = lx + t * w[0], y = ly + t * w[1], z = lz + t * w[2];
+                double sag, g, q;
+                if (!asph_sag(f, c, x * x + y * y, &sag, &g, &q)) return 0;
+                const double F = z - sag;
+                Fp = w[2] - g * (x * w[0] + y * w[1]);
+                if (Fp == 0.0) return 0;
+                const double dt = F / Fp;
+                t -= dt;
+                if (fabs(dt) <= 1e-14 * (1.0 + fabs(t))) { ok = 1; break; }
+            }
+            if (!ok) return 0;
+            if (fabs(Fp) < m[2]) m[2] = fabs(Fp);      /* grazing hit (double root) margin */
+            {
+                const double x = lx + t * w[0], y = ly + t * w[1];
+                double sag, q;
+                if (!asph_sag(f, c, x * x + y * y, &sag, &ga, &q)) return 0;
+            }
+        } else if (R == 0.0 || is_stop) {
             t = -lz / w[2];
         } else {
             const double b = lx * w[0] + ly * w[1] + (lz - R) * w[2];
@@ -133,7 +177,10 @@ static int trace_one(const double* S, int n_surf, const double* L, uint64_t path
         if (k >= K) return 0;              /* sequence exhausted: sigma_{K+1} not the output plane */
         const int is_R = (int)((path_id >> k) & 1ull);
         double nv[3];
-        if (R == 0.0) { nv[0] = 0.0; nv[1] = 0.0; nv[2] = 1.0; }
+        if (asph) {   /* gradient of z - sag(rho): (-g x, -g y, 1), normalised */
+            const double nn = sqrt(ga * ga * (h[0] * h[0] + h[1] * h[1]) + 1.0);
+            nv[0] = -ga * h[0] / nn; nv[1] = -ga * h[1] / nn; nv[2] = 1.0 / nn;
+        } else if (R == 0.0) { nv[0] = 0.0; nv[1] = 0.0; nv[2] = 1.0; }
         else { nv[0] = h[0] / R; nv[1] = h[1] / R; nv[2] = (h[2] - zs - R) / R; }
         if (dot3(nv, w) > 0.0) { nv[0] = -nv[0]; nv[1] = -nv[1]; nv[2] = -nv[2]; }
         const double cosi = -dot3(nv, w);
