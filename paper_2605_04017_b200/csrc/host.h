@@ -27,6 +27,9 @@ struct Surface {
     double z = 0, R = 0, a = 0;
     bool stop = false;
     Glass before, after;
+    // even asphere: conic k and A4, A6, A8, A10
+    bool asph = false;
+    double k = 0, A[4] = {0, 0, 0, 0};
 };
 
 // Thrown inside the host layer, converted to plt_status at the ABI boundary.

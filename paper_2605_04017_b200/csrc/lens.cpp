@@ -60,7 +60,7 @@ void Glass::device_form(int* gform, double g[6]) const {
 // ---------------------------------------------------------------------------
 namespace {
 
-struct Row { double R, t, d; bool stop; Glass g; int line; };
+struct Row { double R, t, d; bool stop; Glass g; int line; bool asph = false; double k = 0, A[4] = {0, 0, 0, 0}; };
 
 bool parse_double(const std::string& s, double* v) {
     if (s.empty()) return false;
@@ -211,6 +211,23 @@ std::vector<Row> rows_from_json(const std::string& text, std::string* name) {
         std::string gs = g && g->t == JVal::kStr ? g->str : (g && g->t == JVal::kNum ? std::to_string(g->num) : "");
         if (gs.empty()) fail(PLT_E_PARSE, "JSON surface " + std::to_string(idx) + ": missing 'glass'");
         r.stop = !parse_glass(gs, nullptr, idx, &r.g);
+        auto conic = it.get("conic");
+        auto asp = it.get("aspheric");
+        if (conic || asp) {
+            r.asph = true;
+            if (conic) {
+                if (conic->t != JVal::kNum) fail(PLT_E_PARSE, "JSON surface " + std::to_string(idx) + ": 'conic' must be a number");
+                r.k = conic->num;
+            }
+            if (asp) {
+                if (asp->t != JVal::kArr || asp->arr.size() > 4)
+                    fail(PLT_E_PARSE, "JSON surface " + std::to_string(idx) + ": 'aspheric' must be [A4, A6, A8, A10]");
+                for (size_t i = 0; i < asp->arr.size(); ++i) {
+                    if (asp->arr[i].t != JVal::kNum) fail(PLT_E_PARSE, "JSON surface " + std::to_string(idx) + ": bad aspheric coefficient");
+                    r.A[i] = asp->arr[i].num;
+                }
+            }
+        }
         rows.push_back(r);
     }
     return rows;
@@ -231,10 +248,22 @@ std::vector<Row> rows_from_table(const std::string& text, std::string* name) {
         while (ls >> t) tok.push_back(t);
         if (tok.empty()) continue;
         if (tok[0] == "name") { if (tok.size() > 1) *name = tok[1]; continue; }
-        if (tok.size() < 4 || tok.size() > 5)
-            fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": expected 'radius thickness glass aperture_diameter [V_d]'");
         Row r{};
         r.line = ln;
+        {   // optional trailing 'asph:k,A4,A6,A8,A10'
+            std::string last = tok.back();
+            std::transform(last.begin(), last.end(), last.begin(), [](unsigned char ch) { return std::tolower(ch); });
+            if (tok.size() > 4 && last.rfind("asph:", 0) == 0) {
+                std::vector<double> v = parse_list(last.substr(5), ln, "asph");
+                if (v.empty() || v.size() > 5) fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": asph needs 1 to 5 numbers (k,A4,A6,A8,A10)");
+                r.asph = true;
+                r.k = v[0];
+                for (size_t i = 1; i < v.size(); ++i) r.A[i - 1] = v[i];
+                tok.pop_back();
+            }
+        }
+        if (tok.size() < 4 || tok.size() > 5)
+            fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": expected 'radius thickness glass aperture_diameter [V_d] [asph:k,A4,...]'");
         if (!parse_double(tok[0], &r.R)) fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": bad radius '" + tok[0] + "'");
         if (!parse_double(tok[1], &r.t)) fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": bad thickness '" + tok[1] + "'");
         if (!parse_double(tok[3], &r.d)) fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": bad aperture '" + tok[3] + "'");
@@ -272,7 +301,14 @@ plt_lens* parse_lens(const char* text, size_t len, const plt_lens_opts* opts) {
         sf.R = r.stop ? 0.0 : r.R;
         sf.before = prev;
         sf.after = r.stop ? prev : r.g;
-        if (!r.stop && sf.R != 0.0 && std::fabs(sf.R) < sf.a)
+        if (r.asph && !r.stop) {
+            sf.asph = true;
+            sf.k = r.k;
+            for (int i = 0; i < 4; ++i) sf.A[i] = r.A[i];
+            const double c = sf.R == 0.0 ? 0.0 : 1.0 / sf.R;
+            if (1.0 - (1.0 + sf.k) * c * c * sf.a * sf.a < 0.0)
+                fail(PLT_E_VALIDATION, where + ": conic surface undefined inside the clear aperture");
+        } else if (!r.stop && sf.R != 0.0 && std::fabs(sf.R) < sf.a)
             fail(PLT_E_VALIDATION, where + ": |radius| < clear semi-aperture (cap would not span the aperture)");
         if (r.stop) { ++nstop; L->stop_index = (int)k; }
         else ++L->n_optical;
@@ -341,6 +377,7 @@ std::vector<Surface> traversal_frame(const plt_lens& L, int dir, double* zS) {
         Surface s = *it;
         s.z = *zS - it->z;
         s.R = it->R == 0.0 ? 0.0 : -it->R;
+        for (int i = 0; i < 4; ++i) s.A[i] = -it->A[i];   // mirrored sag is -sag
         s.before = it->after;
         s.after = it->before;
         m.push_back(s);
@@ -360,6 +397,8 @@ void fill_step(Step<T>* st, const Surface& s, int kind, int is_R, int dir, const
     st->kind = kind;
     st->is_R = is_R;
     st->pad = 0;
+    st->asph[0] = (T)s.k;
+    for (int i = 0; i < 4; ++i) st->asph[1 + i] = (T)s.A[i];
     double g[6];
     far.device_form(&st->gform, g);
     for (int i = 0; i < 6; ++i) st->g[i] = (T)g[i];
@@ -396,7 +435,7 @@ std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, 
         if (k >= K) fail(PLT_E_INVALID_ARG, "path id " + std::to_string(path_id) + " is inconsistent with the lens (interactions exhausted inside the lens)");
         const int isR = (int)((path_id >> k) & 1ull);
         const Glass& far = d > 0 ? sf.after : sf.before;
-        const int kind = sf.R == 0.0 ? kPlane : kSphere;
+        const int kind = sf.asph ? kAsphere : (sf.R == 0.0 ? kPlane : kSphere);
         fill_step(&cp->pf.st[ns], sf, kind, isR, d, far);
         fill_step(&cp->pd.st[ns], sf, kind, isR, d, far);
         ++ns;
@@ -426,6 +465,8 @@ std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, 
         P.flip = dir == PLT_BACKWARD;
         P.has_rect = rect;
         P.has_housing = H > 0;
+        P.has_asph = 0;
+        for (int i = 0; i < ns; ++i) P.has_asph |= P.st[i].kind == kAsphere;
         P.z_out = (T)z_out;
         P.z_mirror = (T)zS;
         P.housing = (T)H;

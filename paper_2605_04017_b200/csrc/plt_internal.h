@@ -18,7 +18,7 @@ namespace plt {
 // ---------------------------------------------------------------------------
 constexpr int kMaxSteps = 72;   // four-bounce paths of a 13-surface lens: <= 61 interactions + stop crossings
 
-enum StepKind : int { kSphere = 0, kPlane = 1, kStop = 2 };
+enum StepKind : int { kSphere = 0, kPlane = 1, kStop = 2, kAsphere = 3 };
 enum GlassForm : int { kCauchyForm = 0, kSellmeier = 1 };
 
 // Guard band of the float32 trace on geometric edges (mm); see trace.cu.
@@ -39,6 +39,7 @@ struct Step {
     int is_R;   // interaction: 0 = T (refract), 1 = R (reflect)
     int gform;  // GlassForm
     int pad;
+    T asph[5];  // kAsphere: conic k, A4, A6, A8, A10 (sag in the traversal frame; c = invR)
 };
 
 template <typename T>
@@ -48,7 +49,7 @@ struct Program {
     int flip;         // 1 for PLT_BACKWARD: input dz and plane are mirrored, output dz negated
     int has_rect;
     int has_housing;
-    int pad;
+    int has_asph;     // any kAsphere step (selects the kernel instantiation with the Newton code)
     T z_out;          // output plane in the traversal frame
     T z_mirror;       // zS for the backward frame (z' = zS - z)
     T housing;        // housing radius

@@ -131,7 +131,7 @@ __device__ __forceinline__ void ray_init2(const Program<float>& P, Ray2& r, m2 a
 // One step S_{L_k, sigma_k} of Eq. 5 on a ray pair (O4-O7).  `st` may be a compile-time
 // constant (the JIT-specialised kernels pass literal steps: branches on kind / is_R /
 // glass form and every lens constant fold away) or a __grid_constant__ program entry.
-template <class PP>   // Program<float>, or the JIT's constexpr header (has_housing, housing2, band_h)
+template <bool kAsph, class PP>   // PP: Program<float>, or the JIT's constexpr header (has_housing, housing2, band_h)
 __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox, f2& oy, f2& oz,
                                       f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
                                       m2& alive, m2& near) {
@@ -144,8 +144,42 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
 #endif
     // O5 intersection
     const f2 lz = oz - mk(st.z);
-    f2 t;
-    if (st.kind != kSphere) {
+    f2 t, ga = mk(0.f);
+    if (kAsph && st.kind == kAsphere) {
+        // even asphere (NEXT-4): 6 Newton steps on F(t) = z - sag(rho) from the tangent plane
+        // (both lanes, no early exit); a lane whose last step is not below the tolerance, or
+        // that hits near-grazing, is flagged for the float64 re-trace
+        const f2 c = mk(st.invR), k1c2 = mk((1.f + st.asph[0]) * st.invR * st.invR);
+        const f2 A4 = mk(st.asph[1]), A6 = mk(st.asph[2]), A8 = mk(st.asph[3]), A10 = mk(st.asph[4]);
+        const f2 B4 = mk(4.f * st.asph[1]), B6 = mk(6.f * st.asph[2]), B8 = mk(8.f * st.asph[3]),
+                 B10 = mk(10.f * st.asph[4]);
+        t = -lz * rcp2(wz);
+        f2 dt = mk(0.f), Fp = mk(1.f);
+        m2 dom{true, true};
+#pragma unroll 1
+        for (int it = 0; it < 6; ++it) {
+            const f2 x = fma2(t, wx, ox), y = fma2(t, wy, oy), z = fma2(t, wz, lz);
+            const f2 r2 = fma2(x, x, y * y);
+            const f2 q = fma2(-k1c2, r2, mk(1.f));
+            dom = dom & le(mk(0.f), q);
+            const f2 sq = sqrt2(mk(fmaxf(q.v.x, 1e-30f), fmaxf(q.v.y, 1e-30f)));
+            const f2 poly = fma2(r2, fma2(r2, fma2(r2, A10, A8), A6), A4);
+            const f2 sag = fma2(c * r2, rcp2(sq + mk(1.f)), (r2 * r2) * poly);
+            const f2 dpoly = fma2(r2, fma2(r2, fma2(r2, B10, B8), B6), B4);
+            const f2 g = fma2(c, rcp2(sq), r2 * dpoly);
+            Fp = fma2(-g, fma2(x, wx, y * wy), wz);
+            dt = (z - sag) * rcp2(Fp);
+            t = t - dt;
+        }
+        alive = alive & dom;
+        const f2 tolt = mk(2e-6f) * (mk(1.f) + abs2(t));
+        near = near | (alive & (lt(tolt, abs2(dt)) | lt(abs2(Fp), mk(1e-3f))));
+        const f2 x = fma2(t, wx, ox), y = fma2(t, wy, oy), r2 = fma2(x, x, y * y);
+        const f2 q = fma2(-k1c2, r2, mk(1.f));
+        alive = alive & le(mk(0.f), q);
+        ga = fma2(c, rcp2(sqrt2(mk(fmaxf(q.v.x, 1e-30f), fmaxf(q.v.y, 1e-30f)))),
+                  r2 * fma2(r2, fma2(r2, fma2(r2, B10, B8), B6), B4));
+    } else if (st.kind != kSphere) {
         t = -lz * rcp2(wz);
     } else {
         const f2 b = fma2(ox, wx, fma2(oy, wy, (lz - mk(st.R)) * wz));
@@ -176,7 +210,10 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     // O7 interaction (sign of the normal folded into g, as in ray_steps)
     f2 nx, ny, nz;
     if (st.kind == kSphere) { nx = ox * mk(st.invR); ny = oy * mk(st.invR); nz = fma2(oz - mk(st.z), mk(st.invR), mk(-1.f)); }
-    else { nx = mk(0.f); ny = mk(0.f); nz = mk(1.f); }
+    else if (kAsph && st.kind == kAsphere) {   // gradient of z - sag: (-g x, -g y, 1), normalised
+        const f2 inv = rsqrt2(fma2(ga * ga, fma2(ox, ox, oy * oy), mk(1.f)));
+        nx = -(ga * ox) * inv; ny = -(ga * oy) * inv; nz = inv;
+    } else { nx = mk(0.f); ny = mk(0.f); nz = mk(1.f); }
     const f2 wn = fma2(nx, wx, fma2(ny, wy, nz * wz));
     const f2 cosi = abs2(wn);
     // air on the far side (constant n = 1): n2 = 1 and eta = ncur exactly
@@ -213,26 +250,28 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
 
 // Steps [s0, s1) of the program (the generic, runtime-indexed path).  The warp leaves the
 // loop once every lane is dead (warp-uniform; no divergent exits).
+template <bool kAsph>
 __device__ __forceinline__ void ray_steps2(const Program<float>& P, Ray2& r, int s0, int s1) {
     f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;
     m2 alive = r.alive, near = r.near;
     for (int s = s0; s < s1; ++s) {
         if (!__any_sync(0xffffffffu, any2(alive))) break;
-        step2(P.st[s], P, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near);
+        step2<kAsph>(P.st[s], P, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near);
     }
     r.ox = ox; r.oy = oy; r.oz = oz; r.wx = wx; r.wy = wy; r.wz = wz; r.I = I; r.ncur = ncur;
     r.alive = alive; r.near = near;
 }
 
 // Step policy of the generic kernel: phases [0, split) and [split, n_steps) of P.
+template <bool kAsph>
 struct GenericSteps {
     __device__ __forceinline__ static bool compact(const Program<float>& P) {
         return P.split > 0 && P.split < P.n_steps;
     }
     __device__ __forceinline__ static void run(const Program<float>& P, Ray2& r, int phase) {
         const bool c = compact(P);
-        if (phase == 0) ray_steps2(P, r, 0, c ? P.split : P.n_steps);
-        else ray_steps2(P, r, P.split, P.n_steps);
+        if (phase == 0) ray_steps2<kAsph>(P, r, 0, c ? P.split : P.n_steps);
+        else ray_steps2<kAsph>(P, r, P.split, P.n_steps);
     }
 };
 
@@ -370,10 +409,11 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
 
 #ifndef PLT_JIT
 // The generic packed kernel (runtime path program).
+template <bool kAsph>
 __global__ void __launch_bounds__(kBlock) trace_kernel_x2(const __grid_constant__ Program<float> P, plt_rays in,
                                                           plt_hits out, int64_t n, Scratch scr,
                                                           const __grid_constant__ SplatCtx sc) {
-    trace_x2_body<GenericSteps>(P, in, out, n, scr, sc);
+    trace_x2_body<GenericSteps<kAsph>>(P, in, out, n, scr, sc);
 }
 #endif
 

@@ -88,7 +88,9 @@ std::string gen_phase(const Program<float>& P, int s0, int s1) {
              lit(st.invR) + ", " + lit(st.a2) + ", " + lit(st.band_a) + ", " + lit(st.sdir) + ", {";
         for (int k = 0; k < 6; ++k) c += lit(st.g[k]) + (k < 5 ? ", " : "");
         c += "}, " + std::to_string(st.kind) + ", " + std::to_string(st.is_R) + ", " + std::to_string(st.gform) +
-             ", 0};\n              step2(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+             ", 0, {";
+        for (int k = 0; k < 5; ++k) c += lit(st.asph[k]) + (k < 4 ? ", " : "");
+        c += "}};\n              step2<true>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
     }
     c += "        } while (0);\n";
     return c;

@@ -3,6 +3,7 @@ symbol include/plt.h declares, its host-only logic (parsing, validation, ABCD,
 ghost enumeration) agrees with the oracle, and compute calls fail loudly without
 an sm_100a device (no CPU fallback)."""
 import ctypes as C
+import json
 import math
 import os
 import re
@@ -189,3 +190,32 @@ def test_camera_entry_points_validate_then_fail_loudly(plt):
     assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, 10, None) == 6
     assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), float("nan"), 10, None) == 1
     assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, -1, None) == 1
+
+
+ASPH_TABLE = """name asph_singlet
+0       5.0  stop                     16.0
+50.0    5.0  sellmeier:1.03961212,0.231792344,1.01046945,0.00600069867,0.0200179144,103.560653  25.0  asph:-0.8,2e-6,-3e-9
+-50.0   0.0  air                      25.0
+"""
+
+
+def test_aspheric_lens_parse_validate_and_match_oracle(plt):
+    """Even aspheres (NEXT-4): the table 'asph:' token and the JSON conic/aspheric fields
+    give the same lens; paraxial data (ABCD) ignore the aspheric terms; a conic undefined
+    inside the aperture is rejected; ghost enumeration unchanged."""
+    L = plt.Lens(ASPH_TABLE)
+    base = plt.Lens(ASPH_TABLE.replace("  asph:-0.8,2e-6,-3e-9", ""))
+    assert L.info()["abcd"] == base.info()["abcd"]
+    O = oracle.load_lens(ASPH_TABLE)
+    assert O.surfaces[1].asph and O.surfaces[1].k == -0.8 and O.surfaces[1].A == (2e-6, -3e-9, 0.0, 0.0)
+    doc = {"name": "j", "surfaces": [
+        {"radius_mm": 0.0, "thickness_mm": 5.0, "glass": "stop", "semi_aperture_mm": 8.0},
+        {"radius_mm": 50.0, "thickness_mm": 5.0, "semi_aperture_mm": 12.5, "conic": -0.8, "aspheric": [2e-6, -3e-9],
+         "glass": "sellmeier:1.03961212,0.231792344,1.01046945,0.00600069867,0.0200179144,103.560653"},
+        {"radius_mm": -50.0, "thickness_mm": 0.0, "glass": "air", "semi_aperture_mm": 12.5}]}
+    J = plt.Lens(json.dumps(doc))
+    assert J.info() == L.info()
+    with pytest.raises(plt.PltError) as e:                 # hyperbolic domain: 1 - (1+k) c^2 a^2 < 0
+        plt.Lens(ASPH_TABLE.replace("asph:-0.8", "asph:20"))
+    assert e.value.status == 3
+    assert L.enumerate_ghosts(2) == base.enumerate_ghosts(2)
