@@ -117,6 +117,15 @@ PLT_API plt_status plt_lens_info(const plt_lens* lens, double lambda_nm, int* n_
                          double abcd[4], double* efl_mm, double* bfl_mm, double* sensor_z_mm);
 
 /*
+ * Paraxial entrance / exit pupils at lambda_nm (lens frame, mm): the aperture stop imaged
+ * through the surfaces in front of it / behind it (backward camera
+ * rays aimed at the exit pupil instead of the rear clear aperture waste fewer samples).
+ * Errors: PLT_E_INVALID_ARG (null), PLT_E_VALIDATION (no stop).
+ */
+PLT_API plt_status plt_lens_pupils(const plt_lens* lens, double lambda_nm, double* entrance_z_mm,
+                                   double* entrance_r_mm, double* exit_z_mm, double* exit_r_mm);
+
+/*
  * Path ids ("Each sequence can be converted to a binary number"):
  * id = 2^K + sum_k 2^(k-1) [interaction k is R], the stop is not an interaction.
  * The all-transmission path of an m-surface lens is 2^m; the two-bounce ghost that

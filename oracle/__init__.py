@@ -38,7 +38,7 @@ import numpy as np
 
 from . import _lib
 from .lens import (OracleLens, all_t_id, decode_path, efl_bfl, encode_path,  # noqa: F401
-                   enumerate_ghosts, ghost_id, mirrored, parse_lens, paraxial_focus_z,
+                   enumerate_ghosts, ghost_id, mirrored, parse_lens, paraxial_focus_z, pupils,
                    surface_array, abcd_vertex_to_vertex, abcd_input_to_plane, glass_index)
 
 FORWARD, BACKWARD = 0, 1

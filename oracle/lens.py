@@ -206,6 +206,44 @@ def abcd_input_to_plane(lens: OracleLens, lam_nm: float, z_in: float, z_out: flo
     return translation_matrix(z_out - lens.surfaces[-1].z) @ M @ translation_matrix(lens.surfaces[0].z - z_in)
 
 
+def pupils(lens: OracleLens, lam_nm: float):
+    """Paraxial entrance and exit pupils (images of the aperture stop through the front and
+    rear groups; SURVEY §8(f) NEXT-3 exit-pupil sampling).  Returns (z_ent, r_ent, z_exit,
+    r_exit) in the lens frame.  Rear group: M from the stop plane to the last vertex; the
+    stop's image lies s' = -B/D behind the last vertex with magnification det(M)/D = 1/D
+    (air).  Front group: N from the first vertex to the stop plane; the object plane
+    conjugate to the stop (A s + B = 0 for N T(s)) is at z = z_first + B/A, imaged onto the
+    stop with magnification A."""
+    surfs = lens.surfaces
+    k = next((i for i, x in enumerate(surfs) if x.is_stop), None)
+    if k is None:
+        raise ValueError("lens has no aperture stop")
+    zs, a = surfs[k].z, surfs[k].a
+
+    def group(ss, z_from):
+        M, z = np.eye(2), z_from
+        for x in ss:
+            M = translation_matrix(x.z - z) @ M
+            M = refraction_matrix(glass_index(x.glass_before, lam_nm), glass_index(x.glass_after, lam_nm), x.R) @ M
+            z = x.z
+        return M, z
+
+    rear = [x for x in surfs[k + 1:] if not x.is_stop]
+    if rear:
+        M, zl = group(rear, zs)
+        z_exit, r_exit = zl - M[0, 1] / M[1, 1], a / abs(M[1, 1])
+    else:
+        z_exit, r_exit = zs, a
+    front = [x for x in surfs[:k] if not x.is_stop]
+    if front:
+        N, zl = group(front, front[0].z)
+        N = translation_matrix(zs - zl) @ N
+        z_ent, r_ent = front[0].z + N[0, 1] / N[0, 0], a / abs(N[0, 0])
+    else:
+        z_ent, r_ent = zs, a
+    return z_ent, r_ent, z_exit, r_exit
+
+
 # ---------------------------------------------------------------------------
 # O2 path ids (sentinel, LSB-first; SURVEY A9) and O12 ghost enumeration
 # ---------------------------------------------------------------------------

@@ -29,7 +29,7 @@ _STATUS = {0: "PLT_OK", 1: "PLT_E_INVALID_ARG", 2: "PLT_E_PARSE", 3: "PLT_E_VALI
 EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "plt_lens_info",
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
-            "plt_trace_jit_cubin", "plt_shade_plane", "plt_propagate_rays")
+            "plt_trace_jit_cubin", "plt_shade_plane", "plt_propagate_rays", "plt_lens_pupils")
 
 
 class PltError(RuntimeError):
@@ -101,9 +101,11 @@ def load():
     L.plt_trace_jit_cubin.argtypes = [p, u64, i, p, C.c_size_t, C.POINTER(C.c_size_t)]
     L.plt_shade_plane.argtypes = [p, d, p, i, i64, C.c_float, p, i64, p]
     L.plt_propagate_rays.argtypes = [p, p, d, i64, p]
+    L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
-              "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_propagate_rays"):
+              "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_propagate_rays",
+              "plt_lens_pupils"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -166,6 +168,13 @@ class Lens:
         buf = C.create_string_buffer(size.value)
         _check(L.plt_trace_jit_cubin(self._h, int(path_id), direction, buf, size.value, C.byref(size)))
         return buf.raw[:size.value]
+
+    def pupils(self, lambda_nm: float = 587.5618) -> dict:
+        """plt_lens_pupils: paraxial entrance / exit pupil positions and radii (mm)."""
+        v = [C.c_double() for _ in range(4)]
+        _check(load().plt_lens_pupils(self._h, lambda_nm, *[C.byref(x) for x in v]))
+        return {"entrance_z_mm": v[0].value, "entrance_r_mm": v[1].value, "exit_z_mm": v[2].value,
+                "exit_r_mm": v[3].value}
 
     def all_t_id(self) -> int:
         return 1 << self.info()["n_optical"]

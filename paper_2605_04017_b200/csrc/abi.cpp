@@ -93,6 +93,16 @@ plt_status plt_lens_info(const plt_lens* lens, double lambda_nm, int* n_optical,
     PLT_GUARD_END
 }
 
+plt_status plt_lens_pupils(const plt_lens* lens, double lambda_nm, double* ez, double* er, double* xz, double* xr) {
+    PLT_GUARD_BEGIN
+    if (!lens || !ez || !er || !xz || !xr) return set_err(PLT_E_INVALID_ARG, "null argument");
+    double o[4];
+    plt::lens_pupils(*lens, lambda_nm, o);
+    *ez = o[0]; *er = o[1]; *xz = o[2]; *xr = o[3];
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
 plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, double min_throughput, uint64_t* ids,
                                 int32_t* ij_pairs, int capacity, int* count) {
     PLT_GUARD_BEGIN

@@ -71,6 +71,7 @@ namespace plt {
 
 plt_lens* parse_lens(const char* text, size_t len, const plt_lens_opts* opts);  // throws Error
 void lens_abcd(const plt_lens& L, double lambda_nm, double M[4]);
+void lens_pupils(const plt_lens& L, double lambda_nm, double out[4]);   // z_ent, r_ent, z_exit, r_exit
 std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, int dir);  // throws
 std::vector<std::pair<uint64_t, std::pair<int, int>>> enumerate_ghosts(const plt_lens& L, int max_bounces,
                                                                        double min_throughput);

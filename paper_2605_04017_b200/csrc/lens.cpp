@@ -3,6 +3,7 @@
 //
 // Citations: P:n = PAPER.md line n, S:n = SPEC.md line n; readings A1..A30 of
 // SURVEY.md §8(c) are restated in DESIGN.md.
+#include <array>
 #include <algorithm>
 #include <cctype>
 #include <cmath>
@@ -362,6 +363,57 @@ void lens_abcd(const plt_lens& L, double lambda_nm, double M[4]) {
         c = c2; d = d2;
     }
     M[0] = a; M[1] = b; M[2] = c; M[3] = d;
+}
+
+// ---------------------------------------------------------------------------
+// Paraxial pupils: the aperture stop imaged through the rear group (exit pupil: distance
+// s' = -B/D behind the last vertex, magnification 1/D in air) and through the front group
+// (entrance pupil: object plane at z_first + B/A conjugate to the stop, magnification A).
+// ---------------------------------------------------------------------------
+void lens_pupils(const plt_lens& L, double lambda_nm, double out[4]) {
+    if (L.stop_index < 0) fail(PLT_E_VALIDATION, "lens has no aperture stop");
+    const Surface& st = L.surf[(size_t)L.stop_index];
+    // group matrix [[a,b],[c,d]] from plane z0 through surfaces [i0, i1) (stops skipped)
+    auto group = [&](size_t i0, size_t i1, double z0, double* zl) {
+        double a = 1, b = 0, c = 0, d = 1, z = z0;
+        for (size_t k = i0; k < i1; ++k) {
+            const Surface& s = L.surf[k];
+            if (s.stop) continue;
+            const double t = s.z - z;
+            a += t * c; b += t * d;
+            const double n1 = s.before.index(lambda_nm), n2 = s.after.index(lambda_nm);
+            const double p = s.R == 0.0 ? 0.0 : (n1 - n2) / (n2 * s.R), q = n1 / n2;
+            const double c2 = p * a + q * c, d2 = p * b + q * d;
+            c = c2; d = d2;
+            z = s.z;
+        }
+        *zl = z;
+        return std::array<double, 4>{a, b, c, d};
+    };
+    const size_t k = (size_t)L.stop_index;
+    bool rear = false, front = false;
+    for (size_t i = k + 1; i < L.surf.size(); ++i) rear |= !L.surf[i].stop;
+    for (size_t i = 0; i < k; ++i) front |= !L.surf[i].stop;
+    if (front) {
+        double zl;
+        size_t first = 0;
+        while (L.surf[first].stop) ++first;
+        auto N = group(first, k, L.surf[first].z, &zl);
+        const double t = st.z - zl;                 // translate to the stop plane
+        N[0] += t * N[2]; N[1] += t * N[3];
+        out[0] = L.surf[first].z + N[1] / N[0];
+        out[1] = st.a / std::fabs(N[0]);
+    } else {
+        out[0] = st.z; out[1] = st.a;
+    }
+    if (rear) {
+        double zl;
+        auto M = group(k + 1, L.surf.size(), st.z, &zl);
+        out[2] = zl - M[1] / M[3];
+        out[3] = st.a / std::fabs(M[3]);
+    } else {
+        out[2] = st.z; out[3] = st.a;
+    }
 }
 
 // ---------------------------------------------------------------------------

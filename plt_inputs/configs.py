@@ -95,13 +95,17 @@ CONFIGS = {
 }
 
 
-def dof_law(shift_mm: float = 0.0, spp: int | None = None) -> dict:
-    """C3_DOF rays with the sensor moved by shift_mm along z (away from the lens for > 0)."""
+def dof_law(shift_mm: float = 0.0, spp: int | None = None, pupil: tuple | None = None) -> dict:
+    """C3_DOF rays with the sensor moved by shift_mm along z (away from the lens for > 0).
+    pupil = (z_mm, radius_mm) re-aims the rays at another disc, e.g. the lens's exit pupil
+    from plt_lens_pupils (default: the rear clear aperture)."""
     cfg = CONFIGS["C3_DOF"]
     law = dict(cfg["law"])
     law["plane_z"] = law["plane_z"] + shift_mm
     if spp is not None:
         law["spp"] = spp
+    if pupil is not None:
+        law["pupil_z"], law["pupil_r"] = float(pupil[0]), float(pupil[1])
     return law
 
 

@@ -219,3 +219,13 @@ def test_aspheric_lens_parse_validate_and_match_oracle(plt):
         plt.Lens(ASPH_TABLE.replace("asph:-0.8", "asph:20"))
     assert e.value.status == 3
     assert L.enumerate_ghosts(2) == base.enumerate_ghosts(2)
+
+
+@pytest.mark.parametrize("name", ["singlet", "dgauss50", "wide24", "wide22"])
+def test_pupils_match_oracle(plt, name):
+    L, O = plt.Lens(LENSES[name]), oracle.load_lens(LENSES[name])
+    for lam in (486.1327, 587.5618, 656.2725):
+        p = L.pupils(lam)
+        o = oracle.pupils(O, lam)
+        assert np.allclose([p["entrance_z_mm"], p["entrance_r_mm"], p["exit_z_mm"], p["exit_r_mm"]], o,
+                           rtol=1e-12, atol=1e-12)

@@ -92,3 +92,23 @@ def test_dof_map_vs_trace_and_focus_sweep(gpu_lib):
         assert abs(r["sharp_m"] / r["sharp_t"] - 1) <= 0.03
     for key in ("sharp_t", "sharp_m"):      # the object plane focuses ~0.6 mm behind the infinity focus
         assert res[0.6][key] > res[-1.0][key] and res[0.6][key] > res[1.5][key]
+
+
+def test_exit_pupil_sampling_raises_the_valid_fraction(gpu_lib):
+    """Aiming the sensor rays at the paraxial exit pupil (plt_lens_pupils) instead of the rear
+    clear aperture: same lens, many more rays reach the scene."""
+    import torch
+    plt = gpu_lib
+    cfg = C.CONFIGS["C3_DOF"]
+    lens = plt.Lens(C.lens_text("C3_DOF"), **cfg["opts"])
+    pp = lens.pupils()
+    fr = {}
+    for key, pupil in (("rear", None), ("exit", (pp["exit_z_mm"], 1.1 * pp["exit_r_mm"]))):
+        n = cfg["width_px"] * cfg["height_px"] * 16
+        d = plt.rays_to_device(R.gen_rays(C.dof_law(0.0, 16, pupil), cfg["seed"], 0, n))
+        h = plt.alloc_hits(n)
+        plt.trace_rays(lens, lens.all_t_id(), d, h, direction=plt.BACKWARD)
+        torch.cuda.synchronize()
+        fr[key] = float(unpack_mask(h["mask_bits"].cpu().numpy(), n).mean())
+    print(fr)
+    assert fr["exit"] > 5 * fr["rear"] and fr["exit"] > 0.5
