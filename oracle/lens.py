@@ -34,6 +34,10 @@ class Surface:
     asph: bool = False
     k: float = 0.0
     A: tuple = (0.0, 0.0, 0.0, 0.0)
+    # single-layer anti-reflection coating: index n_c, thickness d (um);
+    # a quarter wave at lambda0: d = lambda0 / (4 n_c).  coat_n = 0: bare surface
+    coat_n: float = 0.0
+    coat_d_um: float = 0.0
 
 
 @dataclass
@@ -80,6 +84,12 @@ def _glass_token(tok: str, vd: str | None = None):
     return (GLASS_CONST, (nd, 0, 0, 0, 0, 0))
 
 
+def _coat_token(tok: str):
+    """'coat:n_c,lambda0_nm' -> (n_c, quarter-wave thickness in um)."""
+    n_c, lam0 = [float(x) for x in tok.split(":", 1)[1].split(",")][:2]
+    return n_c, lam0 * 1e-3 / (4.0 * n_c)
+
+
 def _asph_token(tok: str):
     """'asph:k,A4,A6,A8,A10' (missing trailing coefficients are 0)."""
     v = [float(x) for x in tok.split(":", 1)[1].split(",")]
@@ -96,12 +106,16 @@ def parse_lens(text: str, opts: dict | None = None) -> OracleLens:
         doc = json.loads(text)
         name = doc.get("name", name)
         for s in doc["surfaces"]:
+            coat = None
+            if "coating" in s:
+                n_c, lam0 = float(s["coating"]["n"]), float(s["coating"]["lambda0_nm"])
+                coat = (n_c, lam0 * 1e-3 / (4.0 * n_c))
             asph = None
             if "conic" in s or "aspheric" in s:
                 A = tuple((list(map(float, s.get("aspheric", []))) + [0.0] * 4)[:4])
                 asph = (float(s.get("conic", 0.0)), A)
             rows.append((float(s["radius_mm"]), float(s["thickness_mm"]),
-                         _glass_token(str(s["glass"])), 2.0 * float(s["semi_aperture_mm"]), asph))
+                         _glass_token(str(s["glass"])), 2.0 * float(s["semi_aperture_mm"]), asph, coat))
     else:
         for line in text.splitlines():
             body = line.split("#", 1)[0].strip()
@@ -111,19 +125,24 @@ def parse_lens(text: str, opts: dict | None = None) -> OracleLens:
             if tok[0] == "name":
                 name = tok[1]
                 continue
-            asph = None
-            if tok[-1].lower().startswith("asph:"):
-                asph = _asph_token(tok[-1])
+            asph, coat = None, None
+            while len(tok) > 4 and tok[-1].lower().startswith(("asph:", "coat:")):
+                if tok[-1].lower().startswith("asph:"):
+                    asph = _asph_token(tok[-1])
+                else:
+                    coat = _coat_token(tok[-1])
                 tok = tok[:-1]
             vd = tok[4] if len(tok) > 4 else None
-            rows.append((float(tok[0]), float(tok[1]), _glass_token(tok[2], vd), float(tok[3]), asph))
+            rows.append((float(tok[0]), float(tok[1]), _glass_token(tok[2], vd), float(tok[3]), asph, coat))
     surfaces, z, prev = [], 0.0, AIR
-    for (r, t, g, d, asph) in rows:
+    for (r, t, g, d, asph, coat) in rows:
         stop = g is None
         after = prev if stop else g
         sf = Surface(z=z, R=0.0 if stop else r, a=0.5 * d, is_stop=stop, glass_before=prev, glass_after=after)
         if asph is not None and not stop:
             sf.asph, sf.k, sf.A = True, asph[0], asph[1]
+        if coat is not None and not stop:
+            sf.coat_n, sf.coat_d_um = coat
         surfaces.append(sf)
         prev = after
         z += t
@@ -145,12 +164,13 @@ def mirrored(lens: OracleLens) -> list:
     for s in reversed(lens.surfaces):
         out.append(Surface(z=zS - s.z, R=-s.R if s.R != 0.0 else 0.0, a=s.a, is_stop=s.is_stop,
                            glass_before=s.glass_after, glass_after=s.glass_before,
-                           asph=s.asph, k=s.k, A=tuple(-x for x in s.A)))   # sag' = -sag
+                           asph=s.asph, k=s.k, A=tuple(-x for x in s.A),   # sag' = -sag
+                           coat_n=s.coat_n, coat_d_um=s.coat_d_um))
     return out
 
 
 def surface_array(surfs: list) -> np.ndarray:
-    a = np.zeros((len(surfs), 24), dtype=np.float64)
+    a = np.zeros((len(surfs), 26), dtype=np.float64)
     for i, s in enumerate(surfs):
         a[i, 0], a[i, 1], a[i, 2], a[i, 3] = s.z, s.R, s.a, 1.0 if s.is_stop else 0.0
         a[i, 4] = s.glass_before[0]
@@ -160,6 +180,7 @@ def surface_array(surfs: list) -> np.ndarray:
         a[i, 18] = 1.0 if s.asph else 0.0
         a[i, 19] = s.k
         a[i, 20:24] = s.A
+        a[i, 24], a[i, 25] = s.coat_n, s.coat_d_um
     return a
 
 
@@ -284,7 +305,13 @@ def _walk_normal_incidence(lens: OracleLens, path_id: int, lam_nm: float):
             return None
         surf = opt[s]
         n2 = glass_index(surf.glass_after if d > 0 else surf.glass_before, lam_nm)
-        R0 = ((ncur - n2) / (ncur + n2)) ** 2
+        if surf.coat_n > 0.0:   # thin film at normal incidence (same Airy formula as the trace)
+            nc = surf.coat_n
+            a, b = (ncur - nc) / (ncur + nc), (nc - n2) / (nc + n2)
+            cb = math.cos(4.0 * math.pi * nc * surf.coat_d_um / (lam_nm * 1e-3))
+            R0 = (a * a + b * b + 2 * a * b * cb) / (1 + a * a * b * b + 2 * a * b * cb)
+        else:
+            R0 = ((ncur - n2) / (ncur + n2)) ** 2
         if L == "T":
             I *= 1.0 - R0
             ncur = n2

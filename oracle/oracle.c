@@ -18,6 +18,9 @@
  * Everything is written in the order the paper/SURVEY state it; no blocking,
  * fusion or re-ordering.  Arithmetic is IEEE double, no fast-math.
  */
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -55,7 +58,8 @@ double orc_glass_index(int model, const double* c, double lambda_nm)
 /*  [3] is_stop   [4] glass-before model  [5..10] coeffs                       */
 /*  [11] glass-after model  [12..17] coeffs                                    */
 /*  [18] is_asph  [19] conic k  [20..23] A4, A6, A8, A10 (even asphere)        */
-#define ORC_STRIDE 24
+/*  [24] coating index n_c (0 = bare)  [25] coating thickness d (um)          */
+#define ORC_STRIDE 26
 
 /* Lens-level parameters: [0] housing radius (0 = none) [1] z of output plane  */
 /* [2] rect W (0 = none) [3] rect H [4] rect cx [5] rect cy                    */
@@ -193,6 +197,23 @@ static int trace_one(const double* S, int n_surf, const double* L, uint64_t path
         double Rf, cost = 0.0;
         if (kappa < 0.0) {
             Rf = 1.0;  /* total internal reflection */
+        } else if (f[24] > 0.0) {
+            /* single thin film n_c, d between n1 and n2: amplitude      */
+            /* coefficients r_1c, r_c2 per polarisation and the film phase 2 beta =           */
+            /* 4 pi n_c d cos_c / lambda give R = (a^2 + b^2 + 2ab cos 2beta) /                */
+            /* (1 + a^2 b^2 + 2ab cos 2beta) (Airy summation, lossless film)                  */
+            cost = sqrt(kappa);
+            const double nc = f[24], d = f[25], lam_um = lambda * 1e-3;
+            const double sc2 = (n1 / nc) * (n1 / nc) * (1.0 - cosi * cosi);
+            const double cosc = sqrt(fmax(0.0, 1.0 - sc2));
+            const double cb = cos(4.0 * M_PI * nc * d * cosc / lam_um);
+            const double as = (n1 * cosi - nc * cosc) / (n1 * cosi + nc * cosc);
+            const double bs = (nc * cosc - n2 * cost) / (nc * cosc + n2 * cost);
+            const double ap = (nc * cosi - n1 * cosc) / (nc * cosi + n1 * cosc);
+            const double bp = (n2 * cosc - nc * cost) / (n2 * cosc + nc * cost);
+            const double Rs = (as * as + bs * bs + 2.0 * as * bs * cb) / (1.0 + as * as * bs * bs + 2.0 * as * bs * cb);
+            const double Rp = (ap * ap + bp * bp + 2.0 * ap * bp * cb) / (1.0 + ap * ap * bp * bp + 2.0 * ap * bp * cb);
+            Rf = 0.5 * (Rs + Rp);
         } else {
             cost = sqrt(kappa);
             const double rs = (n1 * cosi - n2 * cost) / (n1 * cosi + n2 * cost);
