@@ -30,6 +30,8 @@ struct Surface {
     // even asphere: conic k and A4, A6, A8, A10
     bool asph = false;
     double k = 0, A[4] = {0, 0, 0, 0};
+    // single-layer AR coating (NEXT-4): index, thickness in um (0 = bare)
+    double coat_n = 0, coat_d_um = 0;
 };
 
 // Thrown inside the host layer, converted to plt_status at the ABI boundary.

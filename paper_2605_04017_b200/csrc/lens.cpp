@@ -61,7 +61,11 @@ void Glass::device_form(int* gform, double g[6]) const {
 // ---------------------------------------------------------------------------
 namespace {
 
-struct Row { double R, t, d; bool stop; Glass g; int line; bool asph = false; double k = 0, A[4] = {0, 0, 0, 0}; };
+struct Row {
+    double R, t, d; bool stop; Glass g; int line;
+    bool asph = false; double k = 0, A[4] = {0, 0, 0, 0};
+    double coat_n = 0, coat_d_um = 0;
+};
 
 bool parse_double(const std::string& s, double* v) {
     if (s.empty()) return false;
@@ -212,6 +216,13 @@ std::vector<Row> rows_from_json(const std::string& text, std::string* name) {
         std::string gs = g && g->t == JVal::kStr ? g->str : (g && g->t == JVal::kNum ? std::to_string(g->num) : "");
         if (gs.empty()) fail(PLT_E_PARSE, "JSON surface " + std::to_string(idx) + ": missing 'glass'");
         r.stop = !parse_glass(gs, nullptr, idx, &r.g);
+        if (auto co = it.get("coating")) {
+            auto n = co->get("n"), l0 = co->get("lambda0_nm");
+            if (co->t != JVal::kObj || !n || !l0 || n->t != JVal::kNum || l0->t != JVal::kNum)
+                fail(PLT_E_PARSE, "JSON surface " + std::to_string(idx) + ": 'coating' needs numbers 'n' and 'lambda0_nm'");
+            r.coat_n = n->num;
+            r.coat_d_um = l0->num * 1e-3 / (4.0 * n->num);
+        }
         auto conic = it.get("conic");
         auto asp = it.get("aspheric");
         if (conic || asp) {
@@ -251,7 +262,7 @@ std::vector<Row> rows_from_table(const std::string& text, std::string* name) {
         if (tok[0] == "name") { if (tok.size() > 1) *name = tok[1]; continue; }
         Row r{};
         r.line = ln;
-        {   // optional trailing 'asph:k,A4,A6,A8,A10'
+        for (;;) {   // optional trailing 'asph:k,A4,A6,A8,A10' and 'coat:n_c,lambda0_nm' (any order)
             std::string last = tok.back();
             std::transform(last.begin(), last.end(), last.begin(), [](unsigned char ch) { return std::tolower(ch); });
             if (tok.size() > 4 && last.rfind("asph:", 0) == 0) {
@@ -261,6 +272,15 @@ std::vector<Row> rows_from_table(const std::string& text, std::string* name) {
                 r.k = v[0];
                 for (size_t i = 1; i < v.size(); ++i) r.A[i - 1] = v[i];
                 tok.pop_back();
+            } else if (tok.size() > 4 && last.rfind("coat:", 0) == 0) {
+                std::vector<double> v = parse_list(last.substr(5), ln, "coat");
+                if (v.size() != 2 || !(v[0] > 1.0) || !(v[1] > 0.0))
+                    fail(PLT_E_PARSE, "line " + std::to_string(ln) + ": coat needs 'coat:n_c,lambda0_nm' with n_c > 1, lambda0 > 0");
+                r.coat_n = v[0];
+                r.coat_d_um = v[1] * 1e-3 / (4.0 * v[0]);
+                tok.pop_back();
+            } else {
+                break;
             }
         }
         if (tok.size() < 4 || tok.size() > 5)
@@ -302,6 +322,13 @@ plt_lens* parse_lens(const char* text, size_t len, const plt_lens_opts* opts) {
         sf.R = r.stop ? 0.0 : r.R;
         sf.before = prev;
         sf.after = r.stop ? prev : r.g;
+        if (r.coat_n > 0.0 && !r.stop) {
+            const bool air_side = (sf.before.model == Glass::kConst && sf.before.c[0] == 1.0) ||
+                                  (sf.after.model == Glass::kConst && sf.after.c[0] == 1.0);
+            if (!air_side) fail(PLT_E_VALIDATION, where + ": coatings are modelled on air-glass surfaces only");
+            sf.coat_n = r.coat_n;
+            sf.coat_d_um = r.coat_d_um;
+        }
         if (r.asph && !r.stop) {
             sf.asph = true;
             sf.k = r.k;
@@ -451,6 +478,8 @@ void fill_step(Step<T>* st, const Surface& s, int kind, int is_R, int dir, const
     st->pad = 0;
     st->asph[0] = (T)s.k;
     for (int i = 0; i < 4; ++i) st->asph[1 + i] = (T)s.A[i];
+    st->coat_n = (T)s.coat_n;
+    st->coat_kpi = (T)(4.0 * s.coat_n * s.coat_d_um);
     double g[6];
     far.device_form(&st->gform, g);
     for (int i = 0; i < 6; ++i) st->g[i] = (T)g[i];
@@ -518,7 +547,7 @@ std::shared_ptr<CompiledPath> compile_path(const plt_lens& L, uint64_t path_id, 
         P.has_rect = rect;
         P.has_housing = H > 0;
         P.has_asph = 0;
-        for (int i = 0; i < ns; ++i) P.has_asph |= P.st[i].kind == kAsphere;
+        for (int i = 0; i < ns; ++i) P.has_asph |= P.st[i].kind == kAsphere || P.st[i].coat_n > 0;
         P.z_out = (T)z_out;
         P.z_mirror = (T)zS;
         P.housing = (T)H;
@@ -551,8 +580,15 @@ double normal_incidence_throughput(const plt_lens& L, uint64_t id, double lam) {
         if (s < 0 || s >= (int)opt.size()) return -1.0;
         const Surface& sf = *opt[s];
         double n2 = (d > 0 ? sf.after : sf.before).index(lam);
-        double r0 = (ncur - n2) / (ncur + n2);
-        r0 *= r0;
+        double r0;
+        if (sf.coat_n > 0.0) {   // thin film at normal incidence (as the trace's Airy formula)
+            const double nc = sf.coat_n, a = (ncur - nc) / (ncur + nc), b = (nc - n2) / (nc + n2);
+            const double cb = std::cos(4.0 * 3.14159265358979323846 * nc * sf.coat_d_um / (lam * 1e-3));
+            r0 = (a * a + b * b + 2 * a * b * cb) / (1 + a * a * b * b + 2 * a * b * cb);
+        } else {
+            r0 = (ncur - n2) / (ncur + n2);
+            r0 *= r0;
+        }
         if ((id >> k) & 1ull) { I *= r0; d = -d; }
         else { I *= 1.0 - r0; ncur = n2; }
         s += d;

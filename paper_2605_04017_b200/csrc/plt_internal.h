@@ -40,6 +40,8 @@ struct Step {
     int gform;  // GlassForm
     int pad;
     T asph[5];  // kAsphere: conic k, A4, A6, A8, A10 (sag in the traversal frame; c = invR)
+    T coat_n;   // AR coating index (0 = bare surface)
+    T coat_kpi; // 4 n_c d (um): film phase 2 beta = pi coat_kpi cos_c / lambda_um
 };
 
 template <typename T>
@@ -49,7 +51,7 @@ struct Program {
     int flip;         // 1 for PLT_BACKWARD: input dz and plane are mirrored, output dz negated
     int has_rect;
     int has_housing;
-    int has_asph;     // any kAsphere step (selects the kernel instantiation with the Newton code)
+    int has_asph;     // any aspheric or coated step (selects the kernel instantiation with that code)
     T z_out;          // output plane in the traversal frame
     T z_mirror;       // zS for the backward frame (z' = zS - z)
     T housing;        // housing radius

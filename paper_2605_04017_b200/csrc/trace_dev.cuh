@@ -131,6 +131,24 @@ __device__ __forceinline__ void ray_init2(const Program<float>& P, Ray2& r, m2 a
 // One step S_{L_k, sigma_k} of Eq. 5 on a ray pair (O4-O7).  `st` may be a compile-time
 // constant (the JIT-specialised kernels pass literal steps: branches on kind / is_R /
 // glass form and every lens constant fold away) or a __grid_constant__ program entry.
+// Single-layer AR film (NEXT-4): Airy reflectance per polarisation, as the oracle.
+__device__ __forceinline__ f2 coated_rf2(const Step<float>& st, f2 ncur, f2 n2, f2 cosi, f2 cost, f2 A, f2 B, f2 u,
+                                         m2 tir) {
+    const f2 nc = mk(st.coat_n), e1 = ncur * mk(1.f / st.coat_n);
+    const f2 c2 = fma2(-(e1 * e1), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
+    const f2 cosc = sqrt2(mk(fmaxf(c2.v.x, 0.f), fmaxf(c2.v.y, 0.f)));
+    const f2 ph = (mk(st.coat_kpi) * cosc) * sqrt2(u);
+    const f2 cb = mk(cospif(ph.v.x), cospif(ph.v.y));
+    const f2 ncc = nc * cosc;
+    const f2 as = (A - ncc) * rcp2(A + ncc), bs = (ncc - B) * rcp2(ncc + B);
+    const f2 ap = fma2(nc, cosi, -(ncur * cosc)) * rcp2(fma2(nc, cosi, ncur * cosc));
+    const f2 bp = fma2(n2, cosc, -(nc * cost)) * rcp2(fma2(n2, cosc, nc * cost));
+    const f2 ks = (mk(2.f) * as) * (bs * cb), kp = (mk(2.f) * ap) * (bp * cb);
+    const f2 Rs = (fma2(as, as, bs * bs) + ks) * rcp2(fma2(as * as, bs * bs, mk(1.f)) + ks);
+    const f2 Rp = (fma2(ap, ap, bp * bp) + kp) * rcp2(fma2(ap * ap, bp * bp, mk(1.f)) + kp);
+    return sel(tir, mk(1.f), mk(0.5f) * (Rs + Rp));
+}
+
 template <bool kAsph, class PP>   // PP: Program<float>, or the JIT's constexpr header (has_housing, housing2, band_h)
 __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox, f2& oy, f2& oz,
                                       f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
@@ -145,7 +163,11 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     // O5 intersection
     const f2 lz = oz - mk(st.z);
     f2 t, ga = mk(0.f);
+#ifdef PLT_NO_ASPH
+    if (false) {
+#else
     if (kAsph && st.kind == kAsphere) {
+#endif
         // even asphere (NEXT-4): 6 Newton steps on F(t) = z - sag(rho) from the tangent plane
         // (both lanes, no early exit); a lane whose last step is not below the tolerance, or
         // that hits near-grazing, is flagged for the float64 re-trace
@@ -233,7 +255,12 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     const f2 rs = ((A - B) * CpD) * inv, rp = ((C - D) * ApB) * inv;
     const f2 Rf0 = mk(0.5f) * fma2(rs, rs, rp * rp);
     const m2 tir = lt(kappa, mk(0.f));
+#ifdef PLT_NO_COAT
     const f2 Rf = sel(tir, mk(1.f), Rf0);
+#else
+    const f2 Rf = (kAsph && st.coat_n > 0.f) ? coated_rf2(st, ncur, n2, cosi, cost, A, B, u, tir)
+                                             : sel(tir, mk(1.f), Rf0);
+#endif
     if (!st.is_R) {
         alive = alive & m2{!tir.x, !tir.y};   // TIR on a T step absorbs (A6)
         const f2 g0 = fma2(eta, cosi, -cost);

@@ -90,7 +90,7 @@ std::string gen_phase(const Program<float>& P, int s0, int s1) {
         c += "}, " + std::to_string(st.kind) + ", " + std::to_string(st.is_R) + ", " + std::to_string(st.gform) +
              ", 0, {";
         for (int k = 0; k < 5; ++k) c += lit(st.asph[k]) + (k < 4 ? ", " : "");
-        c += "}};\n              step2<true>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+        c += "}, " + lit(st.coat_n) + ", " + lit(st.coat_kpi) + "};\n              step2<true>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
     }
     c += "        } while (0);\n";
     return c;
@@ -108,6 +108,13 @@ std::string gen_source(const Program<float>& P) {
     const bool compact = P.split > 0 && P.split < P.n_steps;
     std::string src = kPrelude;
     src += "#define PLT_JIT_MINB " + std::to_string(jit_min_blocks()) + "\n";
+    // features the program does not use are compiled out entirely (their mere presence, even
+    // constant-folded, changes the generated code: measured 0.610 vs 0.629 ms on C2)
+    bool coat = false, asph = false;
+    for (int i = 0; i < P.n_steps; ++i) { coat |= P.st[i].coat_n > 0.f; asph |= P.st[i].kind == kAsphere; }
+    if (!coat) src += "#define PLT_NO_COAT 1\n";
+    if (!asph) src += "#define PLT_NO_ASPH 1\n";
+    if (const char* e = std::getenv("PLT_JIT_DEFINES")) src += std::string(e) + "\n";   // developer A/B knob
     for (const char* part : kJitSources) src += part;
     src += "\nnamespace plt {\nstruct JitSteps {\n"
            "    __device__ __forceinline__ static bool compact(const Program<float>&) { return ";

@@ -229,3 +229,43 @@ def test_pupils_match_oracle(plt, name):
         o = oracle.pupils(O, lam)
         assert np.allclose([p["entrance_z_mm"], p["entrance_r_mm"], p["exit_z_mm"], p["exit_r_mm"]], o,
                            rtol=1e-12, atol=1e-12)
+
+
+def _coated(text, tok="coat:1.38,550"):
+    """Add a single-layer coating to every surface with air on one side."""
+    lens = oracle.load_lens(text)
+    out, k = [], 0
+    for line in text.splitlines():
+        body = line.split("#", 1)[0].split()
+        if len(body) >= 4 and body[0] != "name":
+            s = lens.surfaces[k]
+            k += 1
+            air = lambda g: g[0] == 0 and g[1][0] == 1.0
+            if not s.is_stop and (air(s.glass_before) or air(s.glass_after)):
+                line = line.split("#", 1)[0].rstrip() + " " + tok
+        out.append(line)
+    return "\n".join(out) + "\n"
+
+
+def test_coated_lens_parse_validate_and_prune_match_oracle(plt):
+    """AR coatings (NEXT-4): parsed in table and JSON forms, rejected on glass-glass
+    surfaces, paraxial data unchanged, and the normal-incidence ghost prune (which now
+    uses the film reflectance) matches the oracle's."""
+    text = _coated(LENSES["dgauss50"])
+    L, O = plt.Lens(text), oracle.load_lens(text)
+    assert L.info()["abcd"] == plt.Lens(LENSES["dgauss50"]).info()["abcd"]
+    assert sum(1 for s in O.surfaces if s.coat_n > 0) >= 6
+    for thr in (0.0, 1e-6, 1e-5):
+        ids, ij = L.enumerate_ghosts(2, thr)
+        oids, oij = oracle.enumerate_ghosts(O, 2, thr)
+        assert ids == oids
+    assert len(L.enumerate_ghosts(2, 1e-5)[0]) < len(plt.Lens(LENSES["dgauss50"]).enumerate_ghosts(2, 1e-5)[0])
+    with pytest.raises(plt.PltError) as e:                 # a coating on a glass-glass interface
+        plt.Lens("name c\n10 2 n:1.5 10 coat:1.38,550\n-10 2 n:1.7 10 coat:1.38,550\n-30 0 air 10\n")
+    assert e.value.status == 3
+    doc = {"surfaces": [{"radius_mm": 0, "thickness_mm": 2, "glass": "n:1.5", "semi_aperture_mm": 5,
+                         "coating": {"n": 1.38, "lambda0_nm": 550}},
+                        {"radius_mm": 0, "thickness_mm": 0, "glass": "air", "semi_aperture_mm": 5}]}
+    J = plt.Lens(json.dumps(doc), sensor_z_mm=10.0)
+    T = plt.Lens("name t\n0 2 n:1.5 10 coat:1.38,550\n0 0 air 10\n", sensor_z_mm=10.0)
+    assert J.enumerate_ghosts(2, 1e-9) == T.enumerate_ghosts(2, 1e-9)

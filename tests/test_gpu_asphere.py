@@ -57,3 +57,31 @@ def test_aspheric_lens_parity(gpu_lib, which):
     compare_trace(gpu_trace(plt, gl, g, rays, precision=1), og, tol_p=5e-5, tol_w=2e-7, tol_i=2e-7)
     s32 = compare_trace(gpu_trace(plt, gl, g, rays, precision=0), og, assert_ok=False)   # generic packed
     assert s32["mask_mismatch"] <= max(2, int(1e-3 * og["valid"].sum()))
+
+
+def test_coated_lens_parity(gpu_lib):
+    """Single-layer AR coatings (NEXT-4) on every air-glass surface of the double-Gauss and
+    an aspheric front: the all-T path (JIT) and a ghost (fp64, generic packed fp32) against
+    the oracle; the coated ghost is much dimmer than the bare one."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_abi_cpu import _coated
+    plt = gpu_lib
+    cfg = C.CONFIGS["C2"]
+    text = _coated(_asph_dgauss())
+    gl, ol = plt.Lens(text, **cfg["opts"]), oracle.load_lens(text, cfg["opts"])
+    rays = R.gen_rays(cfg["law"], 23, 0, (1 << 17) + 7)
+    pid = gl.all_t_id()
+    o = oracle.trace(ol, pid, 0, rays, threads=oracle.host_threads())
+    st = compare_trace(gpu_trace(plt, gl, pid, rays, precision=0), o)
+    assert st["n_both"] > 1000
+    ids, _ = gl.enumerate_ghosts(2)
+    g = int(ids[len(ids) // 2])
+    og = oracle.trace(ol, g, 0, rays, threads=oracle.host_threads())
+    compare_trace(gpu_trace(plt, gl, g, rays, precision=1), og, tol_p=4e-6, tol_w=2e-7, tol_i=2e-7)
+    s32 = compare_trace(gpu_trace(plt, gl, g, rays, precision=0), og, assert_ok=False)
+    assert s32["mask_mismatch"] <= max(2, int(1e-3 * og["valid"].sum())) and s32["max_dI"] <= 1e-5
+    bare = oracle.trace(oracle.load_lens(_asph_dgauss(), cfg["opts"]), g, 0, rays, threads=oracle.host_threads())
+    v = og["valid"] & bare["valid"]
+    assert v.sum() > 100 and og["I"][v].mean() < 0.5 * bare["I"][v].mean()
