@@ -85,3 +85,27 @@ def test_coated_lens_parity(gpu_lib):
     bare = oracle.trace(oracle.load_lens(_asph_dgauss(), cfg["opts"]), g, 0, rays, threads=oracle.host_threads())
     v = og["valid"] & bare["valid"]
     assert v.sum() > 100 and og["I"][v].mean() < 0.5 * bare["I"][v].mean()
+
+
+def test_backward_aspheric_coated_parity(gpu_lib):
+    """Backward (camera) traces through the 24 mm lens with an aspheric, coated element:
+    the mirrored frame negates the sag (pinned by oracle reciprocity); GPU fp32 (JIT) and
+    fp64 against the oracle."""
+    plt = gpu_lib
+    cfg = C.CONFIGS["C3"]
+    lines, k = [], 0
+    for line in LENSES["wide24"].splitlines():
+        body = line.split("#", 1)[0].split()
+        if len(body) >= 4 and body[0] != "name" and body[2].lower() != "stop" and float(body[0]) != 0.0:
+            k += 1
+            if k == 3:
+                line = line.split("#", 1)[0].rstrip() + " asph:-0.5,3e-5,-1e-7 coat:1.38,550"
+        lines.append(line)
+    text = "\n".join(lines) + "\n"
+    gl, ol = plt.Lens(text, **cfg["opts"]), oracle.load_lens(text, cfg["opts"])
+    rays = R.gen_rays(cfg["law"], 31, 0, (1 << 17) + 3)
+    pid = gl.all_t_id()
+    o = oracle.trace(ol, pid, 1, rays, threads=oracle.host_threads())
+    st = compare_trace(gpu_trace(plt, gl, pid, rays, direction=1, precision=0), o)
+    assert st["n_both"] > 2000
+    compare_trace(gpu_trace(plt, gl, pid, rays, direction=1, precision=1), o, tol_p=4e-6, tol_w=2e-7, tol_i=2e-7)

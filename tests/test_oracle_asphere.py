@@ -167,3 +167,33 @@ def test_rotational_symmetry_and_json_equivalence():
         doc["surfaces"].append(e)
     lj = oracle.load_lens(json.dumps(doc))
     assert [(x.asph, x.k, x.A) for x in lj.surfaces] == [(x.asph, x.k, x.A) for x in lens.surfaces]
+
+
+def test_backward_forward_reciprocity_with_aspheres_and_coatings():
+    """The mirrored (backward) frame negates the aspheric sag (A' = -A, k unchanged) and
+    keeps coatings: backward exit rays of the 24 mm lens with an aspheric, coated element,
+    reversed and traced forward, land back on the sensor points they started from."""
+    cfg = C.CONFIGS["C3"]
+    text = LENSES["wide24"]
+    lines, k = [], 0
+    for line in text.splitlines():
+        body = line.split("#", 1)[0].split()
+        if len(body) >= 4 and body[0] != "name" and body[2].lower() != "stop" and float(body[0]) != 0.0:
+            k += 1
+            if k == 3:
+                line = line.split("#", 1)[0].rstrip() + " asph:-0.5,3e-5,-1e-7 coat:1.38,550"
+        lines.append(line)
+    lens = oracle.load_lens("\n".join(lines) + "\n", cfg["opts"])
+    assert sum(s.asph for s in lens.surfaces) == 1
+    r = R.gen_rays(cfg["law"], 3, 0, 20000)
+    pid = oracle.all_t_id(lens.n_optical)
+    b = oracle.trace(lens, pid, 1, r)
+    v = b["valid"]
+    assert v.sum() > 500
+    back = {"ox": b["px"][v], "oy": b["py"][v], "dx": -b["dx"][v], "dy": -b["dy"][v], "dz": -b["dz"][v],
+            "lambda_nm": np.asarray(r["lambda_nm"][v], np.float64), "plane_z": cfg["opts"]["backward_exit_z_mm"]}
+    f = oracle.trace(lens, pid, 0, back)
+    # forward output plane = the sensor plane of the backward rays
+    assert f["valid"].all()
+    assert np.max(np.abs(f["px"] - r["ox"][v])) < 1e-9 and np.max(np.abs(f["py"] - r["oy"][v])) < 1e-9
+    assert np.max(np.abs(f["I"] - b["I"][v])) < 1e-12                 # reciprocity of the film too
