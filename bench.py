@@ -40,7 +40,7 @@ FILM = {"width_px": 768, "height_px": 512, "channels": 1, "sensor_w_mm": 36.0, "
         "center_x_mm": 0.0, "center_y_mm": 0.0}
 TANH_PER_RAY_CLS, TANH_PER_RAY_REG = 64, 160      # 2x32 classifier, 5x32 regressor hidden units
 MAC_CLS, MAC_REG = 4 * 32 + 32 * 32 + 32, 4 * 32 + 4 * 32 * 32 + 32 * 6
-IO_BYTES_PER_RAY = 6 * 4 + 6 * 4 + 1.0 / 8        # SoA in + SoA out + 1 mask bit
+IO_BYTES_PER_RAY = 5 * 4 + 6 * 4 + 1.0 / 8        # SoA in (ox oy dx dy lambda) + SoA out + 1 mask bit
 MUFU_PER_CLK_PER_SM = 16                           # B200 nominal SFU rate (DESIGN.md roofline)
 FP32_LANES_PER_SM = 128                            # FFMA lanes per SM (DESIGN.md roofline)
 # Algorithmic FP32 FLOPs of the exact trace (counted from the O1-O8
@@ -164,7 +164,8 @@ def workload_config(n: int, ws: int, pid: int) -> dict:
                         "all-T trace + factorised map (fitted weights maps/C2_0.pltmap) + splat"
                         + (" + NCCL film all-reduce" if ws > 1 else ""),
             "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid, "film": "768x512 int64",
-            "l2": "inputs 403 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"}
+            "rays": "(x, y, omega_x, omega_y, lambda) float32 SoA, omega in S^2_+ (P:180; dz completed in-kernel)",
+            "l2": "inputs 335 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"}
 
 
 def make_workload(rank: int, n_per_rank: int):
@@ -172,7 +173,13 @@ def make_workload(rank: int, n_per_rank: int):
     from plt_inputs import rays as R
     cfg = C.CONFIGS["C2"]
     rays = R.gen_rays(cfg["law"], cfg["seed"], rank * n_per_rank, n_per_rank)
-    return cfg, rays
+    return cfg, unit_rays(rays)
+
+
+def unit_rays(rays: dict) -> dict:
+    """The workload's rays in the paper's parameterisation (omega in S^2_+): dz is not
+    stored, the query completes it (include/plt.h) -- 20 B per ray on the wire and in HBM."""
+    return {k: v for k, v in rays.items() if k != "dz"}
 
 
 def oracle_step(olens, blob, rays, pid, threads):
@@ -199,7 +206,7 @@ def cpu_baseline(target_s: float = 12.0):
     chunk = 1 << 20
     done, busy, c = 0, 0.0, 0
     while busy < target_s and c < 64:
-        rays = R.gen_rays(cfg["law"], cfg["seed"], c * chunk, chunk)
+        rays = unit_rays(R.gen_rays(cfg["law"], cfg["seed"], c * chunk, chunk))
         t0 = time.perf_counter()
         oracle_step(olens, blob, rays, pid, threads)
         busy += time.perf_counter() - t0
@@ -224,7 +231,7 @@ def run_reference(args, ws, rank):
     blob = C.fitted_map_blob("C2")
     threads = oracle.host_threads()
     n = args.ref_rays
-    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
+    rays = unit_rays(R.gen_rays(cfg["law"], cfg["seed"], 0, n))
     for _ in range(args.warmup):
         oracle_step(olens, blob, {k: (v[:4096] if k != "plane_z" else v) for k, v in rays.items()}, pid, threads)
     t0 = time.perf_counter()
@@ -261,8 +268,10 @@ def run_plt(args, ws, rank, local):
     stream = torch.cuda.current_stream()
 
     # inputs resident in HBM (device-timed value); pinned host copies for e2e
-    host = {k: torch.from_numpy(rays_np[k]).pin_memory() for k in plt.RAY_KEYS}
-    d_rays = {k: host[k].to(dev) for k in plt.RAY_KEYS}
+    keys = [k for k in plt.RAY_KEYS if k in rays_np]
+    host = {k: torch.from_numpy(rays_np[k]).pin_memory() for k in keys}
+    d_rays = {k: host[k].to(dev) for k in keys}
+    d_rays["dz"] = None
     d_rays["plane_z"] = rays_np["plane_z"]
     h_trace = plt.alloc_hits(n, dev)
     h_map = plt.alloc_hits(n, dev)
@@ -419,7 +428,7 @@ def run_plt(args, ws, rank, local):
         "roofline": roof,
         "kernels": kernels,
         "e2e": {"value": ws * n / e2e_s / 1e6, "unit": UNIT,
-                "h2d_bytes_per_step": 6 * 4 * n, "d2h_bytes_per_step": npx * 8},
+                "h2d_bytes_per_step": 4 * len(keys) * n, "d2h_bytes_per_step": npx * 8},
         "gpu_launches": args.steps * (3 if fused else 5),
         "clocks": clocks,
         "peaks_source": peaks_src,

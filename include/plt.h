@@ -148,7 +148,12 @@ PLT_API plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, d
 
 /* Device SoA input rays: origin (ox, oy, plane_z) in the lens frame, direction
  * (dx, dy, dz) (unit; dz > 0 for PLT_FORWARD, dz < 0 for PLT_BACKWARD), wavelength
- * in nm (caller precondition: 380..780; not checked per ray). */
+ * in nm (caller precondition: 380..780; not checked per ray).
+ * dz may be NULL: the direction is then the hemisphere vector omega in S^2_+ of P:180
+ * given by its (x, y) components, |dz| = sqrt(max(0, 1 - dx^2 - dy^2)) with the sign of
+ * the query direction (+ forward, - backward), completed per ray in the kernel's own
+ * precision (fp32 passes in fp32, float64 passes and the guard-band re-trace in fp64).
+ * A caller holding unit directions then moves 20 instead of 24 bytes per ray. */
 typedef struct {
     const float* ox;
     const float* oy;
@@ -293,6 +298,8 @@ PLT_API plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_m
  * precomputed map): o' = o + ((z_t - z_in)/w_z) w in float32 (round-to-nearest,
  * one fma per coordinate), w and lambda copied.  in->plane_z_mm is z_in; out's arrays
  * (device, n each, may alias in's) receive the rays; out->plane_z_mm is not used.
+ * in->dz NULL: w_z = +-sqrt(max(0, 1 - w_x^2 - w_y^2)) pointing towards z_t; out->dz
+ * may then be NULL too (the output stays in the (dx, dy) parameterisation).
  * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
  */
 PLT_API plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, int64_t n,

@@ -81,6 +81,22 @@ def _f64(rays, k):
     return np.ascontiguousarray(rays[k], dtype=np.float64)
 
 
+def hemisphere_dz(dx, dy, sign: float = 1.0):
+    """z-component of the unit direction omega in S^2_+  given its (x, y)
+    components: sign * sqrt(max(0, 1 - dx^2 - dy^2)), in float64 (include/plt.h: rays
+    passed without dz)."""
+    dx = np.asarray(dx, np.float64)
+    dy = np.asarray(dy, np.float64)
+    return sign * np.sqrt(np.maximum(0.0, 1.0 - dx * dx - dy * dy))
+
+
+def _dz(rays, direction_sign: float):
+    """The rays' dz, or -- absent / None -- the hemisphere completion towards the lens."""
+    if rays.get("dz") is None:
+        return np.ascontiguousarray(hemisphere_dz(rays["dx"], rays["dy"], direction_sign))
+    return _f64(rays, "dz")
+
+
 def trace(lens: OracleLens, path_id: int, direction: int, rays: dict, threads: int = 1) -> dict:
     """Exact float64 trace of ``rays`` (float32 arrays widened) along ``path_id``.
 
@@ -88,7 +104,8 @@ def trace(lens: OracleLens, path_id: int, direction: int, rays: dict, threads: i
     frame and ``margins`` (n, 4) = (geometric edge mm, |kappa|, |disc| mm^2, |w_z|).
     """
     S, L, zS, sgn = _frame(lens, direction)
-    ox, oy, dx, dy, dz, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm"))
+    ox, oy, dx, dy, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "lambda_nm"))
+    dz = _dz(rays, 1.0 if direction == FORWARD else -1.0)
     n = ox.size
     if sgn < 0:
         plane_z = zS - float(rays["plane_z"])
@@ -180,7 +197,8 @@ def map_eval(model, rays: dict, threads: int = 1) -> dict:
     ncl, cd, cW, cB = _head_arrays(m["classifier"])
     nrl, rd, rW, rB = _head_arrays(m["regressor"])
     norm = np.ascontiguousarray(m["norm"])
-    ox, oy, dx, dy, dz, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm"))
+    ox, oy, dx, dy, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "lambda_nm"))
+    dz = _dz(rays, 1.0)            # not used by O10 (the canonical input is (r, w'_x, w'_y, lambda))
     n = ox.size
     valid = np.zeros(n, np.uint8)
     out = np.zeros((n, 6), np.float64)
@@ -232,8 +250,11 @@ def shade_plane(scene: dict, z_hits: float, valid, px, py, dx, dy, dz, I, spp: i
 
 def propagate(rays: dict, z_target: float) -> dict:
     """Free-space propagation to z = z_target in float64 (closed form o + ((z_t - z_0)/w_z) w)."""
-    t = (float(z_target) - float(rays["plane_z"])) / np.asarray(rays["dz"], np.float64)
-    out = {k: np.asarray(rays[k], np.float64).copy() for k in ("dx", "dy", "dz", "lambda_nm")}
+    towards = 1.0 if float(z_target) >= float(rays["plane_z"]) else -1.0
+    dz = _dz(rays, towards)                         # absent dz: omega in S^2_+ towards z_target
+    t = (float(z_target) - float(rays["plane_z"])) / dz
+    out = {k: np.asarray(rays[k], np.float64).copy() for k in ("dx", "dy", "lambda_nm")}
+    out["dz"] = dz.copy()
     out["ox"] = np.asarray(rays["ox"], np.float64) + t * out["dx"]
     out["oy"] = np.asarray(rays["oy"], np.float64) + t * out["dy"]
     out["plane_z"] = float(z_target)

@@ -231,9 +231,10 @@ def _stream(stream):
 
 
 def _rays_struct(rays: dict, n: int) -> Rays:
+    """rays["dz"] may be absent or None: directions in S^2_+ given by (dx, dy)."""
     import torch
     f = torch.float32
-    return Rays(*(_ptr(rays[k], n, f) for k in RAY_KEYS), float(rays["plane_z"]))
+    return Rays(*(_ptr(rays.get(k) if k == "dz" else rays[k], n, f) for k in RAY_KEYS), float(rays["plane_z"]))
 
 
 def _hits_struct(hits: dict, n: int) -> Hits:
@@ -252,12 +253,16 @@ def alloc_hits(n: int, device="cuda", flags: bool = False) -> dict:
     return h
 
 
-def rays_to_device(rays: dict, device="cuda", pin: bool = False) -> dict:
-    """Copy a dict of float32 numpy arrays (plt_inputs format) to device tensors."""
+def rays_to_device(rays: dict, device="cuda", pin: bool = False, with_dz: bool = True) -> dict:
+    """Copy a dict of float32 numpy arrays (plt_inputs format) to device tensors.
+    with_dz=False leaves dz out (None): the kernels complete omega in S^2_+ from (dx, dy)."""
     import numpy as np
     import torch
     out = {}
     for k in RAY_KEYS:
+        if k == "dz" and (not with_dz or rays.get("dz") is None):
+            out[k] = None
+            continue
         t = torch.from_numpy(np.ascontiguousarray(rays[k], dtype=np.float32))
         if pin:
             t = t.pin_memory()

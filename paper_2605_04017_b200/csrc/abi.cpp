@@ -51,7 +51,8 @@ plt_status check_device() {
 }
 
 bool rays_ok(const plt_rays* r) {
-    return r && r->ox && r->oy && r->dx && r->dy && r->dz && r->lambda_nm && std::isfinite(r->plane_z_mm);
+    // dz may be NULL: directions given by their (x, y) components (include/plt.h)
+    return r && r->ox && r->oy && r->dx && r->dy && r->lambda_nm && std::isfinite(r->plane_z_mm);
 }
 bool hits_ok(const plt_hits* h) {
     return h && h->mask_bits && h->px && h->py && h->dx && h->dy && h->dz && h->throughput;
@@ -290,7 +291,7 @@ plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_
     PLT_GUARD_BEGIN
     if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
     if (n == 0) return PLT_OK;
-    if (!rays_ok(in) || !out || !out->ox || !out->oy || !out->dx || !out->dy || !out->dz || !out->lambda_nm ||
+    if (!rays_ok(in) || !out || !out->ox || !out->oy || !out->dx || !out->dy || (in->dz && !out->dz) || !out->lambda_nm ||
         !std::isfinite(z_target_mm))
         return set_err(PLT_E_INVALID_ARG, "null ray pointer or non-finite plane");
     plt_status s = check_device();

@@ -55,7 +55,14 @@ __global__ void __launch_bounds__(kThreads) shade_plane_kernel(ScenePlane sc, do
 __global__ void __launch_bounds__(kThreads) propagate_kernel(plt_rays in, plt_rays out, float z_target, int64_t n) {
     const float z0 = (float)in.plane_z_mm;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
-        const float dx = in.dx[i], dy = in.dy[i], dz = in.dz[i];
+        const float dx = in.dx[i], dy = in.dy[i];
+        float dz;
+        if (in.dz) {
+            dz = in.dz[i];
+        } else {   // omega in S^2_+  given by (dx, dy), pointing towards the target plane
+            const float m = sqrtf(fmaxf(0.f, fmaf(-dx, dx, fmaf(-dy, dy, 1.f))));
+            dz = z_target < z0 ? -m : m;
+        }
         const float t = __fdiv_rn(__fsub_rn(z_target, z0), dz);
         const float lam = in.lambda_nm[i], ox = __fmaf_rn(t, dx, in.ox[i]), oy = __fmaf_rn(t, dy, in.oy[i]);
         // plt_rays carries const pointers; `out` is the caller's writable destination (may alias `in`)
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(plt_rays in, plt_ra
         const_cast<float*>(out.oy)[i] = oy;
         const_cast<float*>(out.dx)[i] = dx;
         const_cast<float*>(out.dy)[i] = dy;
-        const_cast<float*>(out.dz)[i] = dz;
+        if (out.dz) const_cast<float*>(out.dz)[i] = dz;
         const_cast<float*>(out.lambda_nm)[i] = lam;
     }
 }

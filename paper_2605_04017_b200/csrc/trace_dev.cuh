@@ -55,6 +55,20 @@ __device__ __forceinline__ void list_append(const Scratch& scr, bool listed, int
 
 constexpr int kBlock = 256;
 
+// Input direction z-component (include/plt.h): the caller's dz, or -- dz == NULL -- the
+// hemisphere vector omega in S^2_+ of P:180 completed from (dx, dy), with the sign of the
+// query direction (backward inputs travel towards -z before the mirroring).
+__device__ __forceinline__ float load_dz(const plt_rays& in, int64_t i, float dx, float dy, int flip) {
+    if (in.dz) return __ldg(in.dz + i);
+    const float m = sqrtf(fmaxf(0.f, fmaf(-dx, dx, fmaf(-dy, dy, 1.f))));
+    return flip ? -m : m;
+}
+__device__ __forceinline__ double load_dz64(const plt_rays& in, int64_t i, double dx, double dy, int flip) {
+    if (in.dz) return (double)in.dz[i];
+    const double m = sqrt(fmax(0.0, fma(-dx, dx, fma(-dy, dy, 1.0))));
+    return flip ? -m : m;
+}
+
 struct f2 { float2 v; };
 struct m2 { bool x, y; };
 __device__ __forceinline__ f2 mk(float a) { return {make_float2(a, a)}; }
@@ -115,12 +129,18 @@ struct Ray2 {
     m2 alive, near;
 };
 
+// complete: the input carries no dz (include/plt.h, A32) -- w_z = sqrt(1 - w_x^2 - w_y^2) in
+// the traversal frame (towards +z after the backward mirroring), already unit length.
 __device__ __forceinline__ void ray_init2(const Program<float>& P, Ray2& r, m2 alive, f2 ox, f2 oy, float plane_z,
-                                          f2 wx, f2 wy, f2 wz, f2 lam_nm) {
+                                          f2 wx, f2 wy, f2 wz, f2 lam_nm, bool complete) {
     if (P.flip) { wz = -wz; plane_z = P.z_mirror - plane_z; }
-    const f2 inv = rsqrt2(fma2(wx, wx, fma2(wy, wy, wz * wz)));
     r.ox = ox; r.oy = oy; r.oz = mk(plane_z);
-    r.wx = wx * inv; r.wy = wy * inv; r.wz = wz * inv;
+    if (complete) {
+        r.wx = wx; r.wy = wy; r.wz = sqrt2(fma2(-wx, wx, fma2(-wy, wy, mk(1.f))));
+    } else {
+        const f2 inv = rsqrt2(fma2(wx, wx, fma2(wy, wy, wz * wz)));
+        r.wx = wx * inv; r.wy = wy * inv; r.wz = wz * inv;
+    }
     const f2 lum = lam_nm * mk(1e-3f);
     r.l2 = lum * lum;
     r.u = rcp2(r.l2);
@@ -344,16 +364,18 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
         float v[2][6] = {{0.f, 0.f, 0.f, 0.f, 1.f, 550.f}, {0.f, 0.f, 0.f, 0.f, 1.f, 550.f}};
         if (in_range.x) {
             v[0][0] = __ldg(in.ox + ix); v[0][1] = __ldg(in.oy + ix); v[0][2] = __ldg(in.dx + ix);
-            v[0][3] = __ldg(in.dy + ix); v[0][4] = __ldg(in.dz + ix); v[0][5] = __ldg(in.lambda_nm + ix);
+            v[0][3] = __ldg(in.dy + ix); v[0][5] = __ldg(in.lambda_nm + ix);
+            if (in.dz) v[0][4] = __ldg(in.dz + ix);
         }
         if (in_range.y) {
             v[1][0] = __ldg(in.ox + iy); v[1][1] = __ldg(in.oy + iy); v[1][2] = __ldg(in.dx + iy);
-            v[1][3] = __ldg(in.dy + iy); v[1][4] = __ldg(in.dz + iy); v[1][5] = __ldg(in.lambda_nm + iy);
+            v[1][3] = __ldg(in.dy + iy); v[1][5] = __ldg(in.lambda_nm + iy);
+            if (in.dz) v[1][4] = __ldg(in.dz + iy);
         }
         f2 lam = mk(v[0][5], v[1][5]);
         Ray2 r;
         ray_init2(P, r, in_range, mk(v[0][0], v[1][0]), mk(v[0][1], v[1][1]), in.plane_z_mm, mk(v[0][2], v[1][2]),
-                  mk(v[0][3], v[1][3]), mk(v[0][4], v[1][4]), lam);
+                  mk(v[0][3], v[1][3]), mk(v[0][4], v[1][4]), lam, in.dz == nullptr);
         Steps::run(P, r, 0);
         m2 own = in_range;
         int slot_x = tid, slot_y = kBlock + tid;   // position within the block's 512 rays

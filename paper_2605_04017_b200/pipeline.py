@@ -1,7 +1,7 @@
 """Host-resident ray batches: chunked copy/compute overlap on two CUDA streams.
 
 The per-ray query (trace + map + splat) is ~0.11 ns per ray on a B200,
-while moving its 24 B of inputs over PCIe costs ~0.45 ns: a batch that lives in host
+while moving its 20-24 B of inputs over PCIe costs ~0.4 ns: a batch that lives in host
 memory is bound by the host->device copy.  `query_host_batch` splits the batch into
 chunks, copies chunk c+1 on a copy stream while the kernels of chunk c run on the
 compute stream (event-ordered, no host synchronisation), and returns the film to pinned
@@ -14,7 +14,7 @@ from . import RAY_KEYS, eval_map, splat_sensor, trace_rays
 
 
 def _view(d: dict, lo: int, hi: int) -> dict:
-    out = {k: v[lo:hi] for k, v in d.items() if k not in ("plane_z", "mask_bits", "flags")}
+    out = {k: v[lo:hi] for k, v in d.items() if k not in ("plane_z", "mask_bits", "flags") and v is not None}
     if "plane_z" in d:
         out["plane_z"] = d["plane_z"]
     if "mask_bits" in d:
@@ -29,7 +29,8 @@ def query_host_batch(lens, path_id: int, m, host_rays: dict, d_rays: dict, h_tra
                      compute_stream=None, copy_stream=None, copy_done=None, fused: bool = True):
     """Trace + map + splat a batch whose inputs are in (pinned) host memory.
 
-    host_rays: pinned CPU float32 tensors (RAY_KEYS) + "plane_z"; d_rays / h_trace / h_map:
+    host_rays: pinned CPU float32 tensors (RAY_KEYS; "dz" may be absent -- unit directions
+    completed in-kernel, 20 instead of 24 B per ray over PCIe) + "plane_z"; d_rays / h_trace / h_map:
     device buffers of at least the batch size; film: device int64 film (accumulated, not
     cleared); film_host: optional pinned int64 tensor that receives the film.  chunk must
     be a multiple of 32 (mask words).  fused: splat inside the query kernels
@@ -49,11 +50,14 @@ def query_host_batch(lens, path_id: int, m, host_rays: dict, d_rays: dict, h_tra
         hi = min(n, lo + chunk)
         with torch.cuda.stream(xs):
             for k in RAY_KEYS:
-                d_rays[k][lo:hi].copy_(host_rays[k][lo:hi], non_blocking=True)
+                if host_rays.get(k) is not None:   # dz may be absent (unit directions)
+                    d_rays[k][lo:hi].copy_(host_rays[k][lo:hi], non_blocking=True)
             copy_done[c].record(xs)
         cs.wait_event(copy_done[c])
         dv = _view(d_rays, lo, hi)
         dv["plane_z"] = host_rays["plane_z"]
+        if host_rays.get("dz") is None:
+            dv["dz"] = None
         ht, hm = _view(h_trace, lo, hi), _view(h_map, lo, hi)
         spl = {"film_desc": film_desc, "film": film, "weight_scale": weight_scale} if fused else None
         trace_rays(lens, path_id, dv, ht, stream=cs, splat=spl)

@@ -269,3 +269,25 @@ def test_coated_lens_parse_validate_and_prune_match_oracle(plt):
     J = plt.Lens(json.dumps(doc), sensor_z_mm=10.0)
     T = plt.Lens("name t\n0 2 n:1.5 10 coat:1.38,550\n0 0 air 10\n", sensor_z_mm=10.0)
     assert J.enumerate_ghosts(2, 1e-9) == T.enumerate_ghosts(2, 1e-9)
+
+
+def test_rays_without_dz_pass_validation_then_fail_loudly(plt):
+    """plt_rays.dz may be NULL (directions in S^2_+ given by (dx, dy)): the call is
+    not an argument error; it needs the GPU (PLT_E_CUDA).  Other null ray arrays still are
+    PLT_E_INVALID_ARG.  plt_propagate_rays: out->dz may be NULL only when in->dz is."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = plt.load()
+    L = plt.Lens(LENSES["dgauss50"])
+    m = plt.Map(CF.map_blob("C2", 1 << 10))
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    no_dz = plt.Rays(fake[0], fake[1], fake[2], fake[3], None, fake[5], -5.0)
+    no_dx = plt.Rays(fake[0], fake[1], None, fake[3], fake[4], fake[5], -5.0)
+    hits = plt.Hits(*fake[:7], None)
+    assert lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(no_dz), C.byref(hits), 10, None) == 6
+    assert lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(no_dx), C.byref(hits), 10, None) == 1
+    assert lib.plt_eval_map(m.handle, C.byref(no_dz), C.byref(hits), None, 10, None) == 6
+    full = plt.Rays(*fake[:6], -5.0)
+    assert lib.plt_propagate_rays(C.byref(no_dz), C.byref(no_dz), 50.0, 10, None) == 6
+    assert lib.plt_propagate_rays(C.byref(full), C.byref(no_dz), 50.0, 10, None) == 1

@@ -60,7 +60,8 @@ def test_shards_union_equals_global_batch():
     for ws in (2, 4):
         n = 4 * (1 << 20) // ws
         parts = [bench.make_workload(r, n)[1] for r in range(ws)]
-        for k in ("ox", "dz", "lambda_nm"):
+        assert all("dz" not in p for p in parts)   # unit directions, dz completed by the query
+        for k in ("ox", "dx", "lambda_nm"):
             assert np.array_equal(np.concatenate([p[k] for p in parts]), whole[k])
 
 

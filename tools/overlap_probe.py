@@ -34,7 +34,7 @@ def main():
     lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
     pid = lens.all_t_id()
     m = plt.Map(C.fitted_map_blob("C2"), lens=lens)
-    d = {k: torch.from_numpy(rays_np[k]).to(dev) for k in plt.RAY_KEYS}
+    d = {k: torch.from_numpy(rays_np[k]).to(dev) for k in plt.RAY_KEYS if k in rays_np}
     d["plane_z"] = rays_np["plane_z"]
     ht, hm = plt.alloc_hits(n, dev), plt.alloc_hits(n, dev)
     F = bench.FILM
