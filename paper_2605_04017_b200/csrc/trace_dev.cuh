@@ -156,7 +156,7 @@ __device__ __forceinline__ f2 coated_rf2(const Step<float>& st, f2 ncur, f2 n2, 
                                          m2 tir) {
     const f2 nc = mk(st.coat_n), e1 = ncur * mk(1.f / st.coat_n);
     const f2 c2 = fma2(-(e1 * e1), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
-    const f2 cosc = sqrt2(mk(fmaxf(c2.v.x, 0.f), fmaxf(c2.v.y, 0.f)));
+    const f2 cosc = sqrt2(c2);   // sqrt2 clamps at 1e-30 (covers c2 < 0)
     const f2 ph = (mk(st.coat_kpi) * cosc) * sqrt2(u);
     const f2 cb = mk(cospif(ph.v.x), cospif(ph.v.y));
     const f2 ncc = nc * cosc;
@@ -169,7 +169,9 @@ __device__ __forceinline__ f2 coated_rf2(const Step<float>& st, f2 ncur, f2 n2, 
     return sel(tir, mk(1.f), mk(0.5f) * (Rs + Rp));
 }
 
-template <bool kAsph, class PP>   // PP: Program<float>, or the JIT's constexpr header (has_housing, housing2, band_h)
+// kN1 (JIT only): the ray is in air before this step, so ncur == 1 exactly and the
+// products with it are dropped (the packed intrinsics are opaque to constant folding).
+template <bool kAsph, class PP, bool kN1 = false>   // PP: Program<float>, or the JIT's constexpr header
 __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox, f2& oy, f2& oz,
                                       f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
                                       m2& alive, m2& near) {
@@ -204,7 +206,7 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
             const f2 r2 = fma2(x, x, y * y);
             const f2 q = fma2(-k1c2, r2, mk(1.f));
             dom = dom & le(mk(0.f), q);
-            const f2 sq = sqrt2(mk(fmaxf(q.v.x, 1e-30f), fmaxf(q.v.y, 1e-30f)));
+            const f2 sq = sqrt2(q);
             const f2 poly = fma2(r2, fma2(r2, fma2(r2, A10, A8), A6), A4);
             const f2 sag = fma2(c * r2, rcp2(sq + mk(1.f)), (r2 * r2) * poly);
             const f2 dpoly = fma2(r2, fma2(r2, fma2(r2, B10, B8), B6), B4);
@@ -219,7 +221,7 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
         const f2 x = fma2(t, wx, ox), y = fma2(t, wy, oy), r2 = fma2(x, x, y * y);
         const f2 q = fma2(-k1c2, r2, mk(1.f));
         alive = alive & le(mk(0.f), q);
-        ga = fma2(c, rcp2(sqrt2(mk(fmaxf(q.v.x, 1e-30f), fmaxf(q.v.y, 1e-30f)))),
+        ga = fma2(c, rcp2(sqrt2(q)),
                   r2 * fma2(r2, fma2(r2, fma2(r2, B10, B8), B6), B4));
     } else if (st.kind != kSphere) {
         t = -lz * rcp2(wz);
@@ -230,12 +232,16 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
         near = near | (alive & lt(disc, (mk(kBandDisc) * b) * b));
         alive = alive & le(mk(0.f), disc);
         const f2 rt = sqrt2(disc);
-        // q = b >= 0 ? -b - rt : -b + rt
-        const f2 q = -(b + mk(b.v.x >= 0.f ? rt.v.x : -rt.v.x, b.v.y >= 0.f ? rt.v.y : -rt.v.y));
+        // q = -(b + copysign(rt, b)) (b = -0 takes -rt: same root pair {q, c/q} = {-+rt, +-rt})
+        const f2 q = -(b + mk(copysignf(rt.v.x, b.v.x), copysignf(rt.v.y, b.v.y)));
         alive = alive & m2{q.v.x != 0.f, q.v.y != 0.f};
         const f2 t1 = c * rcp2(q);
         const bool neg_R = st.R < 0.f;
+#ifdef PLT_JIT   // a live lane has sign(w_z) = sdir (O4 above), a compile-time constant here
+        const bool cx = (st.sdir > 0.f) != neg_R, cy = cx;                      // pbrt cap rule (A3)
+#else
         const bool cx = (wz.v.x > 0.f) != neg_R, cy = (wz.v.y > 0.f) != neg_R;   // pbrt cap rule (A3)
+#endif
         t = mk(cx ? fminf(q.v.x, t1.v.x) : fmaxf(q.v.x, t1.v.x), cy ? fminf(q.v.y, t1.v.y) : fmaxf(q.v.y, t1.v.y));
     }
     alive = alive & lt(mk(kEpsT), t);
@@ -265,11 +271,11 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     constexpr bool air = false;
 #endif
     const f2 n2 = air ? mk(1.f) : glass_index2(st, u, l2);
-    const f2 eta = air ? ncur : ncur * rcp2(n2);
+    const f2 eta = air ? ncur : (kN1 ? rcp2(n2) : ncur * rcp2(n2));
     const f2 kappa = fma2(-(eta * eta), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
     near = near | (alive & lt(abs2(kappa), mk(kBandKappa)));
-    const f2 cost = sqrt2(mk(fmaxf(kappa.v.x, 0.f), fmaxf(kappa.v.y, 0.f)));
-    const f2 A = ncur * cosi, B = n2 * cost, C = n2 * cosi, D = ncur * cost;
+    const f2 cost = sqrt2(kappa);   // sqrt2 clamps at 1e-30 (kappa < 0 is TIR)
+    const f2 A = kN1 ? cosi : ncur * cosi, B = n2 * cost, C = n2 * cosi, D = kN1 ? cost : ncur * cost;
     const f2 ApB = A + B, CpD = C + D;
     const f2 inv = rcp_approx2(ApB * CpD);
     const f2 rs = ((A - B) * CpD) * inv, rp = ((C - D) * ApB) * inv;

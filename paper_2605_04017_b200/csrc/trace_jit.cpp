@@ -79,10 +79,24 @@ const char* kPrelude =
     "typedef int int32_t; typedef unsigned int uint32_t;\n"
     "typedef long long int64_t; typedef unsigned long long uint64_t;\n";
 
+bool far_side_air(const Step<float>& st) {   // as step2's `air`: constant n = 1 behind the surface
+    return st.gform == kCauchyForm && st.g[0] == 1.f && st.g[1] == 0.f && st.g[2] == 0.f;
+}
+
+// Is the ray in air before step s?  (starts in air; a T step enters the medium behind its
+// surface, an R step or the stop leaves the medium unchanged)
+bool in_air_before(const Program<float>& P, int s) {
+    bool air = true;
+    for (int k = 0; k < s; ++k)
+        if (P.st[k].kind != kStop && !P.st[k].is_R) air = far_side_air(P.st[k]);
+    return air;
+}
+
 std::string gen_phase(const Program<float>& P, int s0, int s1) {
     std::string c = "        do {\n";
     for (int s = s0; s < s1; ++s) {
         const Step<float>& st = P.st[s];
+        const char* n1 = in_air_before(P, s) ? "true" : "false";
         c += "            if (!__any_sync(0xffffffffu, any2(alive))) break;\n";
         c += "            { constexpr Step<float> st{" + lit(st.z) + ", " + lit(st.R) + ", " + lit(st.twoR) + ", " +
              lit(st.invR) + ", " + lit(st.a2) + ", " + lit(st.band_a) + ", " + lit(st.sdir) + ", {";
@@ -90,7 +104,7 @@ std::string gen_phase(const Program<float>& P, int s0, int s1) {
         c += "}, " + std::to_string(st.kind) + ", " + std::to_string(st.is_R) + ", " + std::to_string(st.gform) +
              ", 0, {";
         for (int k = 0; k < 5; ++k) c += lit(st.asph[k]) + (k < 4 ? ", " : "");
-        c += "}, " + lit(st.coat_n) + ", " + lit(st.coat_kpi) + "};\n              step2<true>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+        c += "}, " + lit(st.coat_n) + ", " + lit(st.coat_kpi) + "};\n              step2<true, Hdr, " + std::string(n1) + ">(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
     }
     c += "        } while (0);\n";
     return c;
