@@ -109,6 +109,14 @@ __device__ __forceinline__ f2 sqrt2(f2 x) {                     // as Math<float
     const f2 s = x * r;
     return fma2(mk(0.5f) * r, fma2(-s, s, x), s);
 }
+// sqrt without the clamp, for arguments whose negative / zero values only occur on lanes
+// that are killed (disc < 0, TIR) or flagged for the fp64 re-trace (disc, kappa within
+// their guard bands): the NaN such a lane may carry never reaches an output.
+__device__ __forceinline__ f2 sqrt2_nc(f2 x) {
+    const f2 r = mk(rsqrt_approx1(x.v.x), rsqrt_approx1(x.v.y));
+    const f2 s = x * r;
+    return fma2(mk(0.5f) * r, fma2(-s, s, x), s);
+}
 __device__ __forceinline__ f2 rsqrt2(f2 x) {                    // as Math<float>::rsqrt
     const f2 r = mk(rsqrt_approx1(x.v.x), rsqrt_approx1(x.v.y));
     return r * fma2(mk(-0.5f) * x * r, r, mk(1.5f));
@@ -116,6 +124,9 @@ __device__ __forceinline__ f2 rsqrt2(f2 x) {                    // as Math<float
 __device__ __forceinline__ bool any2(m2 m) { return m.x || m.y; }
 
 __device__ __forceinline__ f2 glass_index2(const Step<float>& st, f2 u, f2 l2) {
+#ifdef PLT_JIT   // Abbe glasses are Cauchy with C = 0: drop the (opaque) multiply by zero
+    if (st.gform == kCauchyForm && st.g[2] == 0.f) return fma2(u, mk(st.g[1]), mk(st.g[0]));
+#endif
     if (st.gform == kCauchyForm) return fma2(u, fma2(u, mk(st.g[2]), mk(st.g[1])), mk(st.g[0]));
     f2 s = mk(1.f);
     s = s + (mk(st.g[0]) * l2) * rcp2(l2 - mk(st.g[3]));
@@ -231,10 +242,11 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
         const f2 disc = fma2(b, b, -c);
         near = near | (alive & lt(disc, (mk(kBandDisc) * b) * b));
         alive = alive & le(mk(0.f), disc);
-        const f2 rt = sqrt2(disc);
-        // q = -(b + copysign(rt, b)) (b = -0 takes -rt: same root pair {q, c/q} = {-+rt, +-rt})
+        const f2 rt = sqrt2_nc(disc);
+        // q = -(b + copysign(rt, b)) (b = -0 takes -rt: same root pair {q, c/q} = {-+rt, +-rt}).
+        // q = 0 (b = disc = 0) needs no test: t is then 0, +-inf or NaN, and the lane dies at
+        // t > eps or at the aperture
         const f2 q = -(b + mk(copysignf(rt.v.x, b.v.x), copysignf(rt.v.y, b.v.y)));
-        alive = alive & m2{q.v.x != 0.f, q.v.y != 0.f};
         const f2 t1 = c * rcp2(q);
         const bool neg_R = st.R < 0.f;
 #ifdef PLT_JIT   // a live lane has sign(w_z) = sdir (O4 above), a compile-time constant here
@@ -274,7 +286,7 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     const f2 eta = air ? ncur : (kN1 ? rcp2(n2) : ncur * rcp2(n2));
     const f2 kappa = fma2(-(eta * eta), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
     near = near | (alive & lt(abs2(kappa), mk(kBandKappa)));
-    const f2 cost = sqrt2(kappa);   // sqrt2 clamps at 1e-30 (kappa < 0 is TIR)
+    const f2 cost = sqrt2_nc(kappa);   // kappa < 0: TIR (T lane dies, R lane takes R = 1)
     const f2 A = kN1 ? cosi : ncur * cosi, B = n2 * cost, C = n2 * cosi, D = kN1 ? cost : ncur * cost;
     const f2 ApB = A + B, CpD = C + D;
     const f2 inv = rcp_approx2(ApB * CpD);
@@ -282,15 +294,18 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     const f2 Rf0 = mk(0.5f) * fma2(rs, rs, rp * rp);
     const m2 tir = lt(kappa, mk(0.f));
 #ifdef PLT_NO_COAT
-    const f2 Rf = sel(tir, mk(1.f), Rf0);
+    const f2 Rf = st.is_R ? sel(tir, mk(1.f), Rf0) : Rf0;   // a T lane with TIR dies below: R unused
 #else
     const f2 Rf = (kAsph && st.coat_n > 0.f) ? coated_rf2(st, ncur, n2, cosi, cost, A, B, u, tir)
-                                             : sel(tir, mk(1.f), Rf0);
+                                             : (st.is_R ? sel(tir, mk(1.f), Rf0) : Rf0);
 #endif
     if (!st.is_R) {
         alive = alive & m2{!tir.x, !tir.y};   // TIR on a T step absorbs (A6)
         const f2 g0 = fma2(eta, cosi, -cost);
-        const f2 g = mk(wn.v.x > 0.f ? -g0.v.x : g0.v.x, wn.v.y > 0.f ? -g0.v.y : g0.v.y);
+        // g = w.n > 0 ? -g0 : g0 as a sign-bit flip (one LOP3 per lane); differs only at
+        // w.n = +0 exactly (a ray exactly tangent to the surface: a measure-zero set)
+        const f2 g = mk(__int_as_float(__float_as_int(g0.v.x) ^ (~__float_as_int(wn.v.x) & 0x80000000)),
+                        __int_as_float(__float_as_int(g0.v.y) ^ (~__float_as_int(wn.v.y) & 0x80000000)));
         wx = fma2(eta, wx, g * nx); wy = fma2(eta, wy, g * ny); wz = fma2(eta, wz, g * nz);
         I = fma2(-I, Rf, I);
         ncur = n2;
