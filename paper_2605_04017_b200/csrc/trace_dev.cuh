@@ -180,12 +180,24 @@ __device__ __forceinline__ f2 coated_rf2(const Step<float>& st, f2 ncur, f2 n2, 
     return sel(tir, mk(1.f), mk(0.5f) * (Rs + Rp));
 }
 
+// Relative index of a step as a polynomial in the ray's wavelength variable (JIT only):
+// eta(u) = n_before(u) / n_behind(u) with u = 1/lambda^2 [um^-2] is smooth over the visible
+// range, so the host fits it (Chebyshev interpolation, checked to ~1 fp32 ulp over
+// 380-780 nm, trace_jit.cpp) as sum_k c_k v^k in v = (u - kEtaU0) * kEtaUS in [-1, 1];
+// the step then needs neither the glass formula, nor the reciprocal of n, nor the
+// running index ncur -- and the Fresnel factors take their eta form (r_s = (eta c_i -
+// c_t)/(eta c_i + c_t), r_p = (c_i - eta c_t)/(c_i + eta c_t), same values).
+struct NoEta { static constexpr bool on = false; static constexpr int deg = 0; float c[1]; };
+template <int D>
+struct EtaPoly { static constexpr bool on = true; static constexpr int deg = D; float c[D + 1]; };
+constexpr float kEtaU0 = 4.3f, kEtaUS = 1.f / 2.7f;   // u in [1.6, 7.0] (lambda 378-791 nm)
+
 // kN1 (JIT only): the ray is in air before this step, so ncur == 1 exactly and the
 // products with it are dropped (the packed intrinsics are opaque to constant folding).
-template <bool kAsph, class PP, bool kN1 = false>   // PP: Program<float>, or the JIT's constexpr header
+template <bool kAsph, class PP, bool kN1 = false, class EP = NoEta>   // PP: Program<float>, or the JIT's header
 __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox, f2& oy, f2& oz,
                                       f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
-                                      m2& alive, m2& near) {
+                                      m2& alive, m2& near, const EP& ep = EP{}, const f2 v = f2{}) {
     // O4 direction sanity
     near = near | (alive & lt(abs2(wz), mk(kBandDir)));
 #ifdef PLT_JIT   // constant program: the sign test and the air shortcut below fold at compile time
@@ -282,12 +294,21 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
 #else
     constexpr bool air = false;
 #endif
-    const f2 n2 = air ? mk(1.f) : glass_index2(st, u, l2);
-    const f2 eta = air ? ncur : (kN1 ? rcp2(n2) : ncur * rcp2(n2));
+    f2 n2 = mk(1.f), eta;
+    if constexpr (EP::on) {
+        eta = mk(ep.c[EP::deg]);
+#pragma unroll
+        for (int k = EP::deg - 1; k >= 0; --k) eta = fma2(eta, v, mk(ep.c[k]));
+    } else {
+        n2 = air ? mk(1.f) : glass_index2(st, u, l2);
+        eta = air ? ncur : (kN1 ? rcp2(n2) : ncur * rcp2(n2));
+    }
     const f2 kappa = fma2(-(eta * eta), fma2(-cosi, cosi, mk(1.f)), mk(1.f));
     near = near | (alive & lt(abs2(kappa), mk(kBandKappa)));
     const f2 cost = sqrt2_nc(kappa);   // kappa < 0: TIR (T lane dies, R lane takes R = 1)
-    const f2 A = kN1 ? cosi : ncur * cosi, B = n2 * cost, C = n2 * cosi, D = kN1 ? cost : ncur * cost;
+    f2 A, B, C, D;   // r_s = (A - B)/(A + B), r_p = (C - D)/(C + D)
+    if constexpr (EP::on) { A = eta * cosi; B = cost; C = cosi; D = eta * cost; }   // both divided by n_behind
+    else { A = kN1 ? cosi : ncur * cosi; B = n2 * cost; C = n2 * cosi; D = kN1 ? cost : ncur * cost; }
     const f2 ApB = A + B, CpD = C + D;
     const f2 inv = rcp_approx2(ApB * CpD);
     const f2 rs = ((A - B) * CpD) * inv, rp = ((C - D) * ApB) * inv;
@@ -308,7 +329,7 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
                         __int_as_float(__float_as_int(g0.v.y) ^ (~__float_as_int(wn.v.y) & 0x80000000)));
         wx = fma2(eta, wx, g * nx); wy = fma2(eta, wy, g * ny); wz = fma2(eta, wz, g * nz);
         I = fma2(-I, Rf, I);
-        ncur = n2;
+        if constexpr (!EP::on) ncur = n2;
     } else {
         const f2 two_wn = wn + wn;
         wx = fma2(-two_wn, nx, wx); wy = fma2(-two_wn, ny, wy); wz = fma2(-two_wn, nz, wz);

@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -92,11 +93,89 @@ bool in_air_before(const Program<float>& P, int s) {
     return air;
 }
 
-std::string gen_phase(const Program<float>& P, int s0, int s1) {
+// ---- eta polynomials (trace_dev.cuh EtaPoly) ---------------------------------------
+// Index behind a step's surface at u = 1/lambda^2 (um^-2), from the same float
+// coefficients the kernels use (glass_index2), evaluated in double.
+double n_behind(const Step<float>& st, double u) {
+    if (st.gform == kCauchyForm) return (double)st.g[0] + u * ((double)st.g[1] + u * (double)st.g[2]);
+    const double l2 = 1.0 / u;
+    double s = 1.0;
+    for (int k = 0; k < 3; ++k) s += (double)st.g[k] * l2 / (l2 - (double)st.g[3 + k]);
+    return std::sqrt(s);
+}
+
+// Step whose far side is the medium the ray is in before step s (-1: air).
+int medium_before(const Program<float>& P, int s) {
+    int m = -1;
+    for (int k = 0; k < s; ++k)
+        if (P.st[k].kind != kStop && !P.st[k].is_R) m = far_side_air(P.st[k]) ? -1 : k;
+    return m;
+}
+
+// Fit eta(u) of step s as sum_k c_k v^k, v = (u - kEtaU0) kEtaUS (the constants of
+// trace_dev.cuh), by interpolation at the Chebyshev nodes of the lowest degree D <= 6
+// whose float-rounded coefficients stay within 1.2e-7 relative of eta on a dense grid of
+// u in [1.6, 7.0]; false if none does.
+bool fit_eta(const Program<float>& P, int s, std::vector<float>& c) {
+    // the device computes v = fma(u, kEtaUS, -kEtaU0 * kEtaUS) with these float constants
+    const float us_f = 1.f / 2.7f, off_f = -4.3f * us_f;
+    const double us = (double)us_f, off = (double)off_f;
+    const int m = medium_before(P, s);
+    auto eta = [&](double v) {
+        const double u = (v - off) / us;
+        const double n1 = m < 0 ? 1.0 : n_behind(P.st[m], u);
+        const double n2 = far_side_air(P.st[s]) ? 1.0 : n_behind(P.st[s], u);
+        return n1 / n2;
+    };
+    for (int D = 0; D <= 6; ++D) {
+        double A[7][8];
+        for (int k = 0; k <= D; ++k) {
+            const double x = std::cos(M_PI * (k + 0.5) / (D + 1));
+            double p = 1.0;
+            for (int j = 0; j <= D; ++j) { A[k][j] = p; p *= x; }
+            A[k][D + 1] = eta(x);
+        }
+        for (int i = 0; i <= D; ++i) {           // Gaussian elimination with partial pivoting
+            int piv = i;
+            for (int r = i + 1; r <= D; ++r) if (std::fabs(A[r][i]) > std::fabs(A[piv][i])) piv = r;
+            for (int j = 0; j <= D + 1; ++j) std::swap(A[i][j], A[piv][j]);
+            for (int r = 0; r <= D; ++r) {
+                if (r == i) continue;
+                const double f = A[r][i] / A[i][i];
+                for (int j = i; j <= D + 1; ++j) A[r][j] -= f * A[i][j];
+            }
+        }
+        c.assign(D + 1, 0.f);
+        for (int i = 0; i <= D; ++i) c[i] = (float)(A[i][D + 1] / A[i][i]);
+        double worst = 0.0;
+        for (int g = 0; g <= 4000; ++g) {
+            const double v = -1.0 + g / 2000.0;
+            double p = c[D];
+            for (int k = D - 1; k >= 0; --k) p = p * v + c[k];
+            worst = std::fmax(worst, std::fabs(p / eta(v) - 1.0));
+        }
+        if (worst <= 1.2e-7) return true;
+    }
+    return false;
+}
+
+// Polynomial eta for every interaction step of P, or empty if any step does not fit
+// (the kernel then evaluates the glass formulas exactly).
+std::vector<std::vector<float>> eta_polys(const Program<float>& P) {
+    std::vector<std::vector<float>> out(P.n_steps);
+    for (int s = 0; s < P.n_steps; ++s) {
+        if (P.st[s].kind == kStop) continue;
+        if (!fit_eta(P, s, out[s])) return {};
+    }
+    return out;
+}
+
+std::string gen_phase(const Program<float>& P, int s0, int s1, const std::vector<std::vector<float>>& polys) {
     std::string c = "        do {\n";
     for (int s = s0; s < s1; ++s) {
         const Step<float>& st = P.st[s];
         const char* n1 = in_air_before(P, s) ? "true" : "false";
+        const bool poly = !polys.empty() && st.kind != kStop;
         c += "            if (!__any_sync(0xffffffffu, any2(alive))) break;\n";
         c += "            { constexpr Step<float> st{" + lit(st.z) + ", " + lit(st.R) + ", " + lit(st.twoR) + ", " +
              lit(st.invR) + ", " + lit(st.a2) + ", " + lit(st.band_a) + ", " + lit(st.sdir) + ", {";
@@ -104,7 +183,17 @@ std::string gen_phase(const Program<float>& P, int s0, int s1) {
         c += "}, " + std::to_string(st.kind) + ", " + std::to_string(st.is_R) + ", " + std::to_string(st.gform) +
              ", 0, {";
         for (int k = 0; k < 5; ++k) c += lit(st.asph[k]) + (k < 4 ? ", " : "");
-        c += "}, " + lit(st.coat_n) + ", " + lit(st.coat_kpi) + "};\n              step2<true, Hdr, " + std::string(n1) + ">(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+        c += "}, " + lit(st.coat_n) + ", " + lit(st.coat_kpi) + "};\n";
+        if (poly) {
+            const std::vector<float>& e = polys[s];
+            c += "              constexpr EtaPoly<" + std::to_string(e.size() - 1) + "> ep{{";
+            for (size_t k = 0; k < e.size(); ++k) c += lit(e[k]) + (k + 1 < e.size() ? ", " : "");
+            c += "}};\n              step2<true, Hdr, " + std::string(n1) + ", EtaPoly<" + std::to_string(e.size() - 1) +
+                 ">>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near, ep, v); }\n";
+        } else {
+            c += "              step2<true, Hdr, " + std::string(n1) +
+                 ">(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+        }
     }
     c += "        } while (0);\n";
     return c;
@@ -126,6 +215,9 @@ std::string gen_source(const Program<float>& P) {
     // constant-folded, changes the generated code: measured 0.610 vs 0.629 ms on C2)
     bool coat = false, asph = false;
     for (int i = 0; i < P.n_steps; ++i) { coat |= P.st[i].coat_n > 0.f; asph |= P.st[i].kind == kAsphere; }
+    // eta polynomials: not for coated programs (the film needs n before and behind)
+    static const bool poly_off = [] { const char* e = std::getenv("PLT_JIT_ETA_POLY"); return e && e[0] == '0'; }();
+    const std::vector<std::vector<float>> polys = (coat || poly_off) ? std::vector<std::vector<float>>{} : eta_polys(P);
     if (!coat) src += "#define PLT_NO_COAT 1\n";
     if (!asph) src += "#define PLT_NO_ASPH 1\n";
     if (const char* e = std::getenv("PLT_JIT_DEFINES")) src += std::string(e) + "\n";   // developer A/B knob
@@ -138,10 +230,12 @@ std::string gen_source(const Program<float>& P) {
            "        constexpr Hdr H{" + std::to_string(P.has_housing) + ", " + lit(P.housing2) + ", " + lit(P.band_h) +
            "};\n"
            "        f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;\n"
-           "        m2 alive = r.alive, near = r.near;\n        if (phase == 0) {\n";
-    src += gen_phase(P, 0, compact ? P.split : P.n_steps);
+           "        m2 alive = r.alive, near = r.near;\n";
+    if (!polys.empty()) src += "        const f2 v = fma2(r.u, mk(kEtaUS), mk(-kEtaU0 * kEtaUS));\n";
+    src += "        if (phase == 0) {\n";
+    src += gen_phase(P, 0, compact ? P.split : P.n_steps, polys);
     src += "        } else {\n";
-    src += gen_phase(P, compact ? P.split : P.n_steps, P.n_steps);
+    src += gen_phase(P, compact ? P.split : P.n_steps, P.n_steps, polys);
     src += "        }\n"
            "        r.ox = ox; r.oy = oy; r.oz = oz; r.wx = wx; r.wy = wy; r.wz = wz; r.I = I; r.ncur = ncur;\n"
            "        r.alive = alive; r.near = near;\n    }\n};\n}  // namespace plt\n"

@@ -1,6 +1,9 @@
 """The run-time specialised trace kernel (trace_jit.cpp, used for all-T paths) against the
 generic packed kernel (PLT_TRACE_JIT=0, run in a subprocess since the switch is read once
-per process): identical masks and guard-band flags, outputs equal to float32 rounding.
+per process): identical masks and guard-band flags, outputs equal up to float32 error
+propagation -- the JIT evaluates each step's relative index eta(lambda) as a fitted
+polynomial (within ~1 ulp, trace_jit.cpp fit_eta) instead of the glass formula and a
+reciprocal, so the two kernels round differently (~1e-5 mm after 10 surfaces).
 Both are parity-checked against the oracle elsewhere (test_gpu_trace.py runs the JIT for
 all-T paths and the generic kernel for ghost paths)."""
 import os
@@ -47,5 +50,5 @@ np.savez({str(out)!r}, **{{k: h[k].cpu().numpy() for k in plt.HIT_KEYS + ("mask_
     torch.cuda.synchronize()
     assert np.array_equal(h["mask_bits"].cpu().numpy(), g["mask_bits"])
     assert np.array_equal(h["flags"].cpu().numpy(), g["flags"])
-    for k, tol in (("px", 1e-5), ("py", 1e-5), ("dx", 1e-6), ("dy", 1e-6), ("dz", 1e-6), ("throughput", 1e-6)):
+    for k, tol in (("px", 4e-5), ("py", 4e-5), ("dx", 4e-6), ("dy", 4e-6), ("dz", 4e-6), ("throughput", 2e-6)):
         assert np.max(np.abs(h[k].cpu().numpy() - g[k])) <= tol, k
