@@ -392,13 +392,25 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
     __shared__ float sm_v[8][kRays];       // ox oy oz wx wy wz I ncur of the survivors
     __shared__ float sm_lam[kRays];
     __shared__ int sm_idx[kRays];
-    __shared__ unsigned sm_mask[kRays / 32];
+    // mask words of the tile, double-buffered when compacting: tile k's words are stored
+    // after the first compaction barrier of tile k+1 (every atomicOr of tile k precedes it),
+    // so warps left without survivors go on to the next tile instead of waiting at an
+    // end-of-tile barrier for the warps that carry the survivors
+    __shared__ unsigned sm_mask[2][kRays / 32];
     __shared__ int sm_wcnt[kBlock / 32];
     __shared__ long long sm_w[kBlock];     // fused splat: per-warp aggregation slots
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool compact = Steps::compact(P);
     const unsigned lt_mask = (1u << lane) - 1u;
-    if (tid < kRays / 32) sm_mask[tid] = 0u;
+    if (tid < kRays / 32) { sm_mask[0][tid] = 0u; sm_mask[1][tid] = 0u; }
+    int buf = 0;
+    int64_t pending = -1;                  // base of the tile whose words sit in sm_mask[buf ^ 1]
+    auto flush = [&](int64_t b, unsigned* words) {   // threads < kRays/32, after a barrier
+        if (b >= 0 && tid < kRays / 32) {
+            if (b + 32 * tid < n) out.mask_bits[(b >> 5) + tid] = words[tid];
+            words[tid] = 0u;
+        }
+    };
     __syncthreads();
     for (int64_t base = (int64_t)blockIdx.x * kRays; base < n; base += (int64_t)gridDim.x * kRays) {
         int64_t ix = base + tid, iy = base + kBlock + tid;
@@ -430,6 +442,7 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
             const unsigned lx = __ballot_sync(0xffffffffu, r.alive.x), ly = __ballot_sync(0xffffffffu, r.alive.y);
             if (lane == 0) sm_wcnt[warp] = __popc(lx) + __popc(ly);
             __syncthreads();
+            flush(pending, sm_mask[buf ^ 1]);   // the previous tile's words are complete
             int before = 0, total = 0;
 #pragma unroll
             for (int w = 0; w < kBlock / 32; ++w) { const int c = sm_wcnt[w]; before += w < warp ? c : 0; total += c; }
@@ -474,12 +487,12 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
         if (own.x) {
             write_out(out, ix, ox_);
             if (out.flags) out.flags[ix] = (uint8_t)nx;
-            if (vx) atomicOr(&sm_mask[slot_x >> 5], 1u << (slot_x & 31));
+            if (vx) atomicOr(&sm_mask[buf][slot_x >> 5], 1u << (slot_x & 31));
         }
         if (own.y) {
             write_out(out, iy, oy_);
             if (out.flags) out.flags[iy] = (uint8_t)ny;
-            if (vy) atomicOr(&sm_mask[slot_y >> 5], 1u << (slot_y & 31));
+            if (vy) atomicOr(&sm_mask[buf][slot_y >> 5], 1u << (slot_y & 31));
         }
         list_append(scr, own.x && nx, ix, lane);
         list_append(scr, own.y && ny, iy, lane);
@@ -489,12 +502,18 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
             splat_warp(sc, sm_w + 32 * warp, own.x && vx && !nx, ox_.px, ox_.py, ox_.dz, ox_.I, cx);
             splat_warp(sc, sm_w + 32 * warp, own.y && vy && !ny, oy_.px, oy_.py, oy_.dz, oy_.I, cy);
         }
-        __syncthreads();
-        if (tid < kRays / 32) {
-            if (base + 32 * tid < n) out.mask_bits[(base >> 5) + tid] = sm_mask[tid];
-            sm_mask[tid] = 0u;
+        if (compact) {
+            pending = base;
+            buf ^= 1;
+        } else {
+            __syncthreads();
+            flush(base, sm_mask[buf]);
+            __syncthreads();   // sm_* reused by the next iteration
         }
-        __syncthreads();   // sm_* reused by the next iteration
+    }
+    if (compact) {
+        __syncthreads();
+        flush(pending, sm_mask[buf ^ 1]);
     }
 }
 
