@@ -342,7 +342,7 @@ def run_plt(args, ws, rank, local):
     from paper_2605_04017_b200.pipeline import query_host_batch
     host_rays = dict(host, plane_z=rays_np["plane_z"])
     copy_stream = torch.cuda.Stream(device=dev)
-    chunk = 1 << 21
+    chunk = args.e2e_chunk
     copy_done = [torch.cuda.Event() for _ in range((n + chunk - 1) // chunk)]
 
     def e2e_step():
@@ -447,6 +447,7 @@ def main():
     ap.add_argument("--rays", type=int, default=1 << 24, help="rays per GPU per step")
     ap.add_argument("--ref-rays", type=int, default=1 << 15, help="rays per oracle step (--impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="rays per H2D chunk of the e2e leg")
     ap.add_argument("--splat", choices=["fused", "separate"], default="fused",
                     help="splat in the query kernels' epilogues (default) or as a separate kernel")
     args = ap.parse_args()
