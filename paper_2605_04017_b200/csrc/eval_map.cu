@@ -18,8 +18,10 @@
 //    halves), so the contraction keeps ~16 mantissa bits; plain bf16 activations
 //    would exceed the 2e-3 output tolerance (SURVEY [B3]);
 //  * biases are folded into the contraction (bf16 hi/mid/lo bias columns in B times a
-//    constant ones A tile shared by all groups in shared memory); epilogue per layer: tcgen05.ld -> tanh.approx -> split
-//    -> tcgen05.st -> named barrier -> one thread issues the next layer's MMAs;
+//    constant ones A tile shared by all groups in shared memory); epilogue per layer:
+//    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> one thread issues the
+//    next layer's MMAs (the classifier's first hidden layer uses the accurate
+//    1 - 2/(1 + 2^(2x log2 e)) instead of tanh.approx);
 //  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs;
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
 //    memory; the regressor only runs on full 128-row tiles of queued rays (plus one
@@ -241,9 +243,10 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8])
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // A operand in TMEM (kind::f16, M = 128): row m = lane m, element k of the row in 32-bit
-// column k/2 (even k in the low half).  Hidden/output layers read K = 80: columns 0-15
-// hold bf16(h) (hi, round-to-nearest), 16-31 the bf16 residual h - hi (lo), 32-39 the
-// constant (1, 1, 1, 0, ..) chunk that multiplies the folded bias hi/mid/lo columns of B.
+// column k/2 (even k in the low half).  Hidden/output layers read K = 64 from TMEM:
+// columns 0-15 hold bf16(h) (hi, round-to-nearest), 16-31 the bf16 residual h - hi (lo);
+// their bias K-step takes its A operand -- rows (1, 1, 1, 0, ...) multiplying the folded
+// bias hi/mid/lo columns of B -- from the shared "ones" tile in shared memory.
 // hi + lo carries ~17 significant bits of h (the residual is exact in fp32 and rounded
 // once); the 3-term bias is exact for an fp32 bias.
 __device__ __forceinline__ uint32_t split_pair(float x0, float x1, uint32_t& lo) {
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const int q = warp & 3;          // TMEM lane quarter
     const int lane = tid & 31;
     GroupSmem& Gs = S.g[g];
-    constexpr uint32_t kTmemCols = 512;   // 32 accumulator + 40 A columns per pipeline
+    constexpr uint32_t kTmemCols = 512;   // 32 accumulator + 32 A columns per pipeline, G <= 8
 
     // ---- setup: barriers, TMEM, weights -------------------------------------------------
     if (tid == 0) {
