@@ -93,6 +93,11 @@ bool in_air_before(const Program<float>& P, int s) {
     return air;
 }
 
+bool verbose() {
+    static const bool v = std::getenv("PLT_JIT_VERBOSE") != nullptr;
+    return v;
+}
+
 // ---- eta polynomials (trace_dev.cuh EtaPoly) ---------------------------------------
 // Index behind a step's surface at u = 1/lambda^2 (um^-2), from the same float
 // coefficients the kernels use (glass_index2), evaluated in double.
@@ -113,9 +118,12 @@ int medium_before(const Program<float>& P, int s) {
 }
 
 // Fit eta(u) of step s as sum_k c_k v^k, v = (u - kEtaU0) kEtaUS (the constants of
-// trace_dev.cuh), by interpolation at the Chebyshev nodes of the lowest degree D <= 6
+// trace_dev.cuh), by interpolation at the Chebyshev nodes of the lowest degree D <= 10
 // whose float-rounded coefficients stay within 1.2e-7 relative of eta on a dense grid of
 // u in [1.6, 7.0]; false if none does.
+// Cauchy / Abbe glasses need degree 3 on 378-791 nm; Sellmeier glasses up to ~9 (their
+// infrared term is a pole of eta(u) at u = 0, just outside the interval).
+constexpr int kMaxEtaDeg = 10;
 bool fit_eta(const Program<float>& P, int s, std::vector<float>& c) {
     // the device computes v = fma(u, kEtaUS, -kEtaU0 * kEtaUS) with these float constants
     const float us_f = 1.f / 2.7f, off_f = -4.3f * us_f;
@@ -127,8 +135,8 @@ bool fit_eta(const Program<float>& P, int s, std::vector<float>& c) {
         const double n2 = far_side_air(P.st[s]) ? 1.0 : n_behind(P.st[s], u);
         return n1 / n2;
     };
-    for (int D = 0; D <= 6; ++D) {
-        double A[7][8];
+    for (int D = 0; D <= kMaxEtaDeg; ++D) {
+        double A[kMaxEtaDeg + 1][kMaxEtaDeg + 2];
         for (int k = 0; k <= D; ++k) {
             const double x = std::cos(M_PI * (k + 0.5) / (D + 1));
             double p = 1.0;
@@ -218,6 +226,12 @@ std::string gen_source(const Program<float>& P) {
     // eta polynomials: not for coated programs (the film needs n before and behind)
     static const bool poly_off = [] { const char* e = std::getenv("PLT_JIT_ETA_POLY"); return e && e[0] == '0'; }();
     const std::vector<std::vector<float>> polys = (coat || poly_off) ? std::vector<std::vector<float>>{} : eta_polys(P);
+    if (verbose()) {
+        std::string d;
+        for (const auto& e : polys) d += e.empty() ? "-" : std::to_string(e.size() - 1);
+        std::fprintf(stderr, "plt: trace JIT eta(lambda): %s\n",
+                     polys.empty() ? "exact glass formulas" : ("polynomial degrees per step " + d).c_str());
+    }
     if (!coat) src += "#define PLT_NO_COAT 1\n";
     if (!asph) src += "#define PLT_NO_ASPH 1\n";
     if (const char* e = std::getenv("PLT_JIT_DEFINES")) src += std::string(e) + "\n";   // developer A/B knob
@@ -258,11 +272,6 @@ std::map<std::string, Entry> g_cache;
 std::string key_of(const Program<float>& P) {
     const size_t bytes = offsetof(Program<float>, st) + sizeof(Step<float>) * (size_t)P.n_steps;
     return std::string(reinterpret_cast<const char*>(&P), bytes);
-}
-
-bool verbose() {
-    static const bool v = std::getenv("PLT_JIT_VERBOSE") != nullptr;
-    return v;
 }
 
 }  // namespace

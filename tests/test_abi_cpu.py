@@ -291,3 +291,18 @@ def test_rays_without_dz_pass_validation_then_fail_loudly(plt):
     full = plt.Rays(*fake[:6], -5.0)
     assert lib.plt_propagate_rays(C.byref(no_dz), C.byref(no_dz), 50.0, 10, None) == 6
     assert lib.plt_propagate_rays(C.byref(full), C.byref(no_dz), 50.0, 10, None) == 1
+
+
+@pytest.mark.parametrize("kind", ["coated", "aspheric", "sellmeier"])
+def test_trace_jit_compiles_for_every_feature(plt, kind):
+    """The run-time specialised trace compiles for programs that use each optional feature:
+    coated surfaces (no eta polynomials: the film needs both indices), aspheres (Newton
+    intersection) and Sellmeier glasses (eta(lambda) fitted from the Sellmeier formula)."""
+    if kind == "coated":
+        L = plt.Lens(_coated(LENSES["dgauss50"]))
+    elif kind == "aspheric":
+        L = plt.Lens(ASPH_TABLE, sensor_z_mm=120.0)
+    else:
+        L = plt.Lens(LENSES["singlet"])
+    cubin = L.trace_jit_cubin(L.all_t_id())
+    assert cubin[:4] == b"\x7fELF" and b"plt_trace_jit" in cubin
