@@ -56,6 +56,7 @@ struct GroupSmem {
     float qc[kQueue], qs[kQueue];            // rotation (cos, sin) to undo
     int qi[kQueue];                          // ray index | reflection flag << 31
     int wcount[4];                           // per-warp valid counts (prefix)
+    int64_t next_tile[2];                    // dynamic scheduler: the group's next tile (by parity)
     long long wsum[kTile];                   // fused splat: per-warp aggregation slots
 };
 
@@ -293,6 +294,7 @@ struct Params {
     MapParams mp;
     const uint8_t* wimg;   // device weight image
     SplatCtx sc;           // fused splat of the valid outputs (sc.film == nullptr: none)
+    int* tile_ctr;         // dynamic tile scheduler: tiles handed out beyond the first G per CTA
 };
 
 // Canonicalisation of §4.1 (Eq. 10): rotate p onto +x, reflect so w'_y >= 0,
@@ -607,14 +609,22 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         qcount -= rows;
     };
 
-    for (int it = 0; tile < P.n_tiles; ++it, tile += group_stride) {
+    // tiles: the first G per CTA statically (tile = group id), then dynamically -- one
+    // atomicAdd per tile hands the next one to whichever pipeline is free, so pipelines
+    // whose tiles held more valid rays (more regressor work) take fewer tiles and the
+    // SMs finish together
+    for (int it = 0; tile < P.n_tiles; ++it) {
         const int st = it & 1;
         const int64_t base = tile * kTile;
         const int64_t i = base + t;
         const bool in_range = i < n;
-        // next tile's inputs -> other stage (its previous contents were consumed a tile ago)
-        const int64_t next = tile + group_stride;
-        if (t == 0 && next < P.n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
+        // claim the next tile and prefetch its inputs into the other stage (its previous
+        // contents were consumed a tile ago); published to the group through next_tile[it & 1]
+        if (t == 0) {
+            const int64_t next = group_stride + (int64_t)atomicAdd(P.tile_ctr, 1);
+            Gs.next_tile[it & 1] = next;
+            if (next < P.n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
+        }
         PLT_CLK(o0);
         float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
         if (tile_full_tma(tile)) {
@@ -667,6 +677,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             Gs.qi[slot] = (int)i | (k.flip ? (int)0x80000000u : 0);
         }
         qcount += total;
+        const int64_t next_tile = Gs.next_tile[it & 1];   // written before the group barrier above
         PLT_CLK(o5);
         if (qcount >= kTile) run_regressor(kTile);
 #ifdef PLT_MAP_PROFILE
@@ -674,6 +685,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         ++pr_tiles; pr_in += o1 - o0; pr_outep += o3 - o2; pr_write += o4 - o3; pr_queue += o5 - o4;
         if (o6 - o5 > 100) { pr_reg += o6 - o5; ++pr_regs; }
 #endif
+        tile = next_tile;
     }
     if (qcount > 0) run_regressor(qcount);
 #ifdef PLT_MAP_PROFILE
@@ -722,6 +734,7 @@ int launch_groups(const Params& P, int sms, cudaStream_t stream) {
 
 int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams& mp, const plt_rays& in,
                     const plt_hits& out, float* raw, int64_t n, void* stream, const SplatCtx& sc) {
+    static thread_local int warm_dev = -1;   // keep the stream-ordered pool's memory (no cudaMalloc per call)
     if (lay.total_bytes > kMaxImageBytes) return (int)cudaErrorInvalidValue;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -743,11 +756,28 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
         return e ? atoi(e) : 8;
     }();
     cudaStream_t s = (cudaStream_t)stream;
-    if (groups == 4) return launch_groups<4>(P, sms, s);
-    if (groups == 6) return launch_groups<6>(P, sms, s);
-    if (groups == 8) return launch_groups<8>(P, sms, s);
-    if (groups == 7) return launch_groups<7>(P, sms, s);
-    return launch_groups<8>(P, sms, s);
+    if (warm_dev != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        warm_dev = dev;
+    }
+    // tile counter from the stream-ordered pool (no host synchronisation; capture-safe)
+    void* ctr = nullptr;
+    cudaError_t e = cudaMallocAsync(&ctr, 256, s);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaMemsetAsync(ctr, 0, 256, s);
+    if (e != cudaSuccess) return (int)e;
+    P.tile_ctr = (int*)ctr;
+    int rc;
+    if (groups == 4) rc = launch_groups<4>(P, sms, s);
+    else if (groups == 6) rc = launch_groups<6>(P, sms, s);
+    else if (groups == 7) rc = launch_groups<7>(P, sms, s);
+    else rc = launch_groups<8>(P, sms, s);
+    const cudaError_t fe = cudaFreeAsync(ctr, s);
+    return rc != 0 ? rc : (int)fe;
 }
 
 }  // namespace plt
