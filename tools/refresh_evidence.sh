@@ -16,4 +16,10 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -k 'regex:plt_trace_jit|refine_kernel|eval_map_kernel' -c 3 -o $out/${tag}_full \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $out/${tag}_ncu_full.log 2>&1 || echo "ncu full failed"
 timeout 900 python tools/configs_bench.py > $out/${tag}_configs.json 2> $out/${tag}_configs.err || echo "configs failed"
+# NEXT-2 flare images and NEXT-3 depth of field (timings + image agreement)
+for c in C4_22 C4_59; do
+    timeout 600 python tools/flare_compare.py --config $c --out $out/${tag}_flare_$c.json --png $out/${tag}_flare_$c \
+        > $out/${tag}_flare_$c.log 2>&1 || echo "flare $c failed"
+done
+timeout 900 python tools/dof_compare.py --out $out/${tag}_dof.json --png $out/${tag}_dof > $out/${tag}_dof.log 2>&1 || echo "dof failed"
 tail -c 400 $out/${tag}_bench.json

@@ -51,6 +51,10 @@ def main(tag):
                 with open(os.path.join(p, f"{tag}_{kind}.json"), "w") as f:
                     json.dump(line, f, indent=1)
                     f.write("\n")
+    for f in sorted(os.listdir(g)):   # flare / dof images and reports
+        if f.startswith(f"{tag}_flare_") or f.startswith(f"{tag}_dof"):
+            if f.endswith(".json") or f.endswith(".png"):
+                shutil.copy(os.path.join(g, f), os.path.join(p, f))
     launches = os.path.join(g, f"{tag}_bench_launches.csv")
     if os.path.exists(launches):
         shutil.copy(launches, os.path.join(p, f"{tag}_bench_launches.csv"))
