@@ -21,5 +21,5 @@ for c in C4_22 C4_59; do
     timeout 600 python tools/flare_compare.py --config $c --out $out/${tag}_flare_$c.json --png $out/${tag}_flare_$c \
         > $out/${tag}_flare_$c.log 2>&1 || echo "flare $c failed"
 done
-timeout 900 python tools/dof_compare.py --out $out/${tag}_dof.json --png $out/${tag}_dof > $out/${tag}_dof.log 2>&1 || echo "dof failed"
+timeout 900 python tools/dof_compare.py --spp 1024 --out $out/${tag}_dof.json --png $out/${tag}_dof > $out/${tag}_dof.log 2>&1 || echo "dof failed"
 tail -c 400 $out/${tag}_bench.json
