@@ -20,7 +20,8 @@
 //  * biases are folded into the contraction (bf16 hi/mid/lo bias columns in B times a
 //    constant ones A tile shared by all groups in shared memory); epilogue per layer:
 //    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> one thread issues the
-//    next layer's MMAs (the classifier's first hidden layer uses the accurate
+//    next layer's MMAs (the 16 most logit-influential units of the classifier's first
+//    hidden layer -- ordered first at map load, map.cpp -- use the accurate
 //    1 - 2/(1 + 2^(2x log2 e)) instead of tanh.approx);
 //  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs;
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
@@ -217,6 +218,9 @@ __device__ __forceinline__ float2 tanh_ex2_newton2(float2 x) {
     for (int it = 0; it < 3; ++it) r = __fmul2_rn(r, __ffma2_rn(nd, r, two));
     return __ffma2_rn(make_float2(-2.f, -2.f), r, one);
 }
+#ifndef PLT_MAP_CLS_ACCURATE_HALVES
+#define PLT_MAP_CLS_ACCURATE_HALVES 1   // halves (16 units) of the classifier h1 with the accurate tanh
+#endif
 #ifndef PLT_MAP_CLS_TANH
 #define PLT_MAP_CLS_TANH 1   // classifier first hidden layer: 0 MUFU tanh, 1 ex2+rcp, 2 rational
 #endif
@@ -508,7 +512,9 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             float v[16];
             tmem_ld16(tmem_row + 16 * half, v);
             PLT_CLK(h1);
-            if (accurate && PLT_MAP_CLS_TANH == 1) {
+            // the classifier's h1 units are ordered by influence on the logit (map.cpp):
+            // the first PLT_MAP_CLS_ACCURATE_HALVES x 16 take the accurate tanh
+            if (accurate && PLT_MAP_CLS_TANH == 1 && half < PLT_MAP_CLS_ACCURATE_HALVES) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = tanh_accurate(v[j]);
             } else if (accurate && PLT_MAP_CLS_TANH == 3) {

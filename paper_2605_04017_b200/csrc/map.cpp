@@ -8,6 +8,8 @@
 // i.e. 8-row x 16-byte core matrices, adjacent along K (LBO = 128 B) and stacked
 // along N (SBO = K/8 * 128 B).  The input layer's operand repeats W along K so one
 // K=16 MMA consumes the exact bf16 hi/mid/lo split of the 4 inputs: k 0..3, 4..7, 8..11 = W.
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -118,6 +120,9 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
     m->image.assign(L.total_bytes, 0);
     float* outw = reinterpret_cast<float*>(m->image.data() + L.out_off);
 
+    // read both heads: per layer W (bf16, [fo][fi]) and b (fp32, [fo])
+    std::vector<uint16_t> Wl[2][6];
+    std::vector<float> bl[2][6];
     for (int head = 0; head < 2; ++head) {
         const int nl = head == 0 ? 3 : 6;
         const int* dims = head == 0 ? cls_dims : reg_dims;
@@ -127,12 +132,48 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
                 fail(PLT_E_VALIDATION, std::string(head ? "regressor" : "classifier") + " layer " + std::to_string(l) +
                                            " has dims " + std::to_string(fi) + "->" + std::to_string(fo) +
                                            ", expected " + std::to_string(dims[l]) + "->" + std::to_string(dims[l + 1]));
-            std::vector<uint16_t> W(fo * fi);
+            std::vector<uint16_t>& W = Wl[head][l];
+            W.resize(fo * fi);
             r.need(2 * W.size(), "weights");
             std::memcpy(W.data(), blob + r.off, 2 * W.size());
             r.off += 2 * W.size();
-            std::vector<float> b(fo);
+            std::vector<float>& b = bl[head][l];
+            b.resize(fo);
             for (uint32_t o = 0; o < fo; ++o) b[o] = r.get<float>("bias");
+        }
+    }
+    // Classifier first hidden layer: order its 32 units by their influence on the logit,
+    // s_j = sum_i |w3_i| |W2_ij| (a bound on d logit / d h1_j), most influential first.
+    // The kernel evaluates the first 16 with the accurate tanh and the rest with MUFU
+    // tanh.approx.  Permuting hidden units (W1 rows, b1,
+    // W2 columns) leaves the network's function unchanged.
+    {
+        const std::vector<uint16_t>&W2 = Wl[0][1], &w3 = Wl[0][2];
+        double sens[32];
+        for (int j = 0; j < 32; ++j) {
+            sens[j] = 0.0;
+            for (int i = 0; i < 32; ++i) sens[j] += std::fabs((double)bf16_to_f(w3[i])) * std::fabs((double)bf16_to_f(W2[i * 32 + j]));
+        }
+        int perm[32];
+        for (int j = 0; j < 32; ++j) perm[j] = j;
+        std::stable_sort(perm, perm + 32, [&](int a, int b) { return sens[a] > sens[b]; });
+        std::vector<uint16_t> W1 = Wl[0][0], W2p = W2;
+        std::vector<float> b1 = bl[0][0];
+        for (int nw = 0; nw < 32; ++nw) {
+            const int od = perm[nw];
+            for (int k = 0; k < 4; ++k) W1[nw * 4 + k] = Wl[0][0][od * 4 + k];
+            b1[nw] = bl[0][0][od];
+            for (int i = 0; i < 32; ++i) W2p[i * 32 + nw] = W2[i * 32 + od];
+        }
+        Wl[0][0] = W1; bl[0][0] = b1; Wl[0][1] = W2p;
+    }
+    for (int head = 0; head < 2; ++head) {
+        const int nl = head == 0 ? 3 : 6;
+        const int* dims = head == 0 ? cls_dims : reg_dims;
+        for (int l = 0; l < nl; ++l) {
+            const uint32_t fo = (uint32_t)dims[l + 1], fi = (uint32_t)dims[l];
+            const std::vector<uint16_t>& W = Wl[head][l];
+            const std::vector<float>& b = bl[head][l];
             if (l + 1 == nl) {   // output layer: fp32 block
                 float* wo = outw + (head == 0 ? kOutClsW : kOutRegW);
                 float* bo = outw + (head == 0 ? kOutClsB : kOutRegB);
