@@ -218,7 +218,8 @@ PLT_API void plt_map_free(plt_map* map);
 PLT_API plt_status plt_eval_map(const plt_map* map, const plt_rays* in, const plt_hits* out,
                         float* raw_out, int64_t n, void* cuda_stream);
 
-/* Film description for sensor splatting (Eq. 8). */
+/* Film description for sensor splatting (Eq. 8).  All sizes > 0 and
+ * channels * height_px * width_px < 2^31 (PLT_E_INVALID_ARG otherwise). */
 typedef struct {
     int width_px, height_px, channels;
     double sensor_w_mm, sensor_h_mm, center_x_mm, center_y_mm;

@@ -124,7 +124,8 @@ plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, double mi
 
 static bool film_desc_ok(const plt_film_desc* fd) {
     return fd && fd->width_px > 0 && fd->height_px > 0 && fd->channels > 0 && fd->sensor_w_mm > 0 &&
-           fd->sensor_h_mm > 0 && std::isfinite(fd->center_x_mm) && std::isfinite(fd->center_y_mm);
+           fd->sensor_h_mm > 0 && std::isfinite(fd->center_x_mm) && std::isfinite(fd->center_y_mm) &&
+           (int64_t)fd->width_px * fd->height_px * fd->channels < ((int64_t)1 << 31);   // 32-bit pixel keys
 }
 
 // Validate a fused-splat target; on success *sc holds the kernel constants.

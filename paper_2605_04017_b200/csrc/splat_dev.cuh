@@ -17,9 +17,11 @@
 
 namespace plt {
 
-// Pixel key (or -1 with drop = true) and fixed-point weight of one valid hit.
-__device__ __forceinline__ long long splat_key(const SplatCtx& c, float px, float py, float dz, float I, int ch,
-                                               long long& w, bool& drop) {
+// Pixel key (or -1 with drop = true) and fixed-point weight of one valid hit.  Films are
+// limited to < 2^31 entries (checked at the ABI), so the key is a 32-bit int and the warp
+// groups lanes with the 32-bit __match_any_sync.
+__device__ __forceinline__ int splat_key(const SplatCtx& c, float px, float py, float dz, float I, int ch,
+                                         long long& w, bool& drop) {
     constexpr float kGuard = 2e-3f;
     // Pixel coordinate: fp32 estimate first.  Its error is < 1e-3 px for any film below
     // 10^5 px, so when it lies more than kGuard from an integer its floor equals the
@@ -34,7 +36,7 @@ __device__ __forceinline__ long long splat_key(const SplatCtx& c, float px, floa
     }
     if (fxf >= 0.0 && fxf < (double)c.width && fyf >= 0.0 && fyf < (double)c.height && ch < c.channels) {
         w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn((double)I, fabs((double)dz)), (double)c.scale), 4294967296.0));
-        return ((long long)ch * c.height + (long long)fyf) * c.width + (long long)fxf;
+        return (ch * c.height + (int)fyf) * c.width + (int)fxf;
     }
     drop = true;
     return -1;
@@ -47,7 +49,8 @@ __device__ __forceinline__ long long splat_key(const SplatCtx& c, float px, floa
 __device__ __forceinline__ void splat_warp(const SplatCtx& c, long long* wsm, bool hit, float px, float py,
                                            float dz, float I, int ch) {
     const int lane = threadIdx.x & 31;
-    long long key = -1, w = 0;
+    int key = -1;
+    long long w = 0;
     bool drop = false;
     if (hit) key = splat_key(c, px, py, dz, I, ch, w, drop);
     wsm[lane] = w;
