@@ -306,3 +306,19 @@ def test_trace_jit_compiles_for_every_feature(plt, kind):
         L = plt.Lens(LENSES["singlet"])
     cubin = L.trace_jit_cubin(L.all_t_id())
     assert cubin[:4] == b"\x7fELF" and b"plt_trace_jit" in cubin
+
+
+def test_film_size_limit(plt):
+    """Splat keys are 32-bit: films with channels*height*width >= 2^31 are rejected before
+    any device work (PLT_E_INVALID_ARG), smaller ones pass validation (then need the GPU)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = plt.load()
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    hits = plt.Hits(*fake[:7], None)
+    big = plt.FilmDesc(65536, 32768, 1, 24.0, 16.0, 0.0, 0.0)      # 2^31 entries
+    ok = plt.FilmDesc(65535, 32768, 1, 24.0, 16.0, 0.0, 0.0)
+    film = C.c_void_p(1 << 20)
+    assert lib.plt_splat_sensor(C.byref(big), film, C.byref(hits), None, 1.0, 10, None, None) == 1
+    assert lib.plt_splat_sensor(C.byref(ok), film, C.byref(hits), None, 1.0, 10, None, None) == 6
