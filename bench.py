@@ -136,13 +136,20 @@ def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional-test knob only (never for timing): PLT_BENCH_SHARE_GPU=1 maps every rank
+    # onto the visible GPUs round-robin and uses gloo, so the multi-rank code path can be
+    # exercised on a one-GPU box (the ranks' kernels never wait on each other)
+    share = os.environ.get("PLT_BENCH_SHARE_GPU") == "1"
     if args.impl == "plt":
+        if share:
+            local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if args.impl == "plt" else "gloo",
-                                device_id=torch.device("cuda", local) if args.impl == "plt" else None)
+        nccl = args.impl == "plt" and not share
+        dist.init_process_group("nccl" if nccl else "gloo",
+                                device_id=torch.device("cuda", local) if nccl else None)
     return ws, rank, local
 
 
@@ -160,12 +167,15 @@ def ncu_traffic(kernel: str):
 
 def workload_config(n: int, ws: int, pid: int) -> dict:
     """The `config` object shared by both arms (same workload, metric and unit)."""
-    return {"workload": "C2: 50 mm double-Gauss (Kolb/pbrt stand-in), 2^24 rays per GPU, lambda U[400,700] nm, "
+    size = f"2^{n.bit_length() - 1}" if n & (n - 1) == 0 else str(n)
+    return {"workload": f"C2: 50 mm double-Gauss (Kolb/pbrt stand-in), {size} rays per GPU, lambda U[400,700] nm, "
                         "all-T trace + factorised map (fitted weights maps/C2_0.pltmap) + splat"
                         + (" + NCCL film all-reduce" if ws > 1 else ""),
             "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid, "film": "768x512 int64",
             "rays": "(x, y, omega_x, omega_y, lambda) float32 SoA, omega in S^2_+ (P:180; dz completed in-kernel)",
-            "l2": "inputs 335 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"dp{ws} over rays"}
+            "l2": (f"inputs {20 * n / 1e6:.0f} MB/GPU > 126 MB L2 (no flush needed)" if 20 * n > 126e6
+                   else f"inputs {20 * n / 1e6:.0f} MB/GPU fit in L2 (not a contract workload size)"),
+            "parallelism": f"dp{ws} over rays"}
 
 
 def make_workload(rank: int, n_per_rank: int):
