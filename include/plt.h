@@ -150,7 +150,7 @@ PLT_API plt_status plt_enumerate_ghosts(const plt_lens* lens, int max_bounces, d
  * (dx, dy, dz) (unit; dz > 0 for PLT_FORWARD, dz < 0 for PLT_BACKWARD), wavelength
  * in nm (caller precondition: 380..780; not checked per ray -- the run-time
  * specialised fp32 trace evaluates each surface's relative index as a polynomial fitted
- * on 378..791 nm, so rays outside the precondition get extrapolated indices).
+ * on 378..791 nm and sends rays outside that range to its exact float64 re-trace).
  * dz may be NULL: the direction is then the hemisphere vector omega in S^2_+ of P:180
  * given by its (x, y) components, |dz| = sqrt(max(0, 1 - dx^2 - dy^2)) with the sign of
  * the query direction (+ forward, - backward), completed per ray in the kernel's own

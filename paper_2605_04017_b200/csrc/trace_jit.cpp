@@ -245,7 +245,11 @@ std::string gen_source(const Program<float>& P) {
            "};\n"
            "        f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;\n"
            "        m2 alive = r.alive, near = r.near;\n";
-    if (!polys.empty()) src += "        const f2 v = fma2(r.u, mk(kEtaUS), mk(-kEtaU0 * kEtaUS));\n";
+    if (!polys.empty()) {
+        src += "        const f2 v = fma2(r.u, mk(kEtaUS), mk(-kEtaU0 * kEtaUS));\n";
+        // rays outside the fitted wavelength range go to the exact float64 re-trace
+        src += "        if (phase == 0) near = near | (alive & (lt(v, mk(-1.f)) | lt(mk(1.f), v)));\n";
+    }
     src += "        if (phase == 0) {\n";
     src += gen_phase(P, 0, compact ? P.split : P.n_steps, polys);
     src += "        } else {\n";

@@ -52,3 +52,25 @@ np.savez({str(out)!r}, **{{k: h[k].cpu().numpy() for k in plt.HIT_KEYS + ("mask_
     assert np.array_equal(h["flags"].cpu().numpy(), g["flags"])
     for k, tol in (("px", 4e-5), ("py", 4e-5), ("dx", 4e-6), ("dy", 4e-6), ("dz", 4e-6), ("throughput", 2e-6)):
         assert np.max(np.abs(h[k].cpu().numpy() - g[k])) <= tol, k
+
+
+def test_jit_out_of_range_wavelengths_take_the_exact_retrace(gpu_lib):
+    """The JIT evaluates each step's relative index as a polynomial fitted on 378-791 nm;
+    rays outside that range must be flagged for the float64 re-trace (exact glass
+    formulas) and still match the oracle."""
+    import oracle
+    from gpu_helpers import compare_trace, gpu_trace
+    plt = gpu_lib
+    cfg = C.CONFIGS["C2"]
+    gl = plt.Lens(C.lens_text("C2"), **cfg["opts"])
+    ol = oracle.load_lens(C.lens_text("C2"), cfg["opts"])
+    rays = R.gen_rays(cfg["law"], 23, 0, 1 << 16)
+    lam = rays["lambda_nm"].copy()
+    lam[0::3] = 350.0
+    lam[1::3] = 850.0
+    rays["lambda_nm"] = lam
+    g = gpu_trace(plt, gl, gl.all_t_id(), rays)
+    o = oracle.trace(ol, gl.all_t_id(), 0, rays, threads=oracle.host_threads())
+    compare_trace(g, o)
+    out = (lam < 378.0) | (lam > 791.0)
+    assert np.all(g["flags"][out] == 1)
