@@ -101,3 +101,46 @@ LENSES = {
     "wide24": WIDE24,
     "dgauss59": DGAUSS59,
 }
+
+
+def random_lens_text(seed: int) -> tuple:
+    """A seeded random air-spaced lens for fuzz parity tests: 2-3 elements, each a singlet
+    or a cemented doublet, a stop between two of them; radii |R| in [25, 150] mm of either
+    sign, clear semi-apertures <= 0.55 |R| (so every cap is a proper spherical cap), glass
+    2-6 mm, air 0.5-5 mm; glasses Abbe (n_d 1.48-1.85, V_d 25-65), Cauchy or the N-BK7
+    Sellmeier.  Returns (text, front semi-aperture mm, z of the last vertex mm).  DATA only:
+    no optics is evaluated here."""
+    import numpy as np
+    rng = np.random.default_rng([int(seed), 0x1E75])
+    bk7 = "sellmeier:1.03961212,0.231792344,1.01046945,0.00600069867,0.0200179144,103.560653"
+
+    def glass():
+        k = rng.integers(0, 3)
+        if k == 0:
+            return f"abbe:{rng.uniform(1.48, 1.85):.4f},{rng.uniform(25, 65):.1f}"
+        if k == 1:
+            return f"cauchy:{rng.uniform(1.45, 1.75):.4f},{rng.uniform(0.003, 0.012):.5f},0"
+        return bk7
+
+    semi = float(rng.uniform(6.0, 11.0))
+    rows, z = [], 0.0
+    n_el = int(rng.integers(2, 4))
+    stop_after = int(rng.integers(0, n_el - 1))
+    for e in range(n_el):
+        n_surf = 2 if rng.random() < 0.6 else 3            # singlet or cemented doublet
+        for s in range(n_surf):
+            R = float(rng.uniform(25.0, 150.0)) * (1 if rng.random() < 0.5 else -1)
+            R = max(abs(R), semi / 0.55) * np.sign(R)
+            last = s == n_surf - 1
+            if last:
+                t, g = float(rng.uniform(0.5, 5.0)), "air"
+            else:
+                t, g = float(rng.uniform(2.0, 6.0)), glass()
+            rows.append([R, t, g, 2.0 * semi])
+        if e == stop_after:
+            rows.append([0.0, float(rng.uniform(1.0, 4.0)), "stop", 2.0 * semi * 0.8])
+    rows[-1][1] = 0.0
+    for r in rows[:-1]:
+        z += r[1]
+    text = "name fuzz_%d\n" % seed + "".join(f"{r[0]:.4f} {r[1]:.4f} {r[2]} {r[3]:.4f}\n" for r in rows)
+    return text, semi, z

@@ -322,3 +322,19 @@ def test_film_size_limit(plt):
     film = C.c_void_p(1 << 20)
     assert lib.plt_splat_sensor(C.byref(big), film, C.byref(hits), None, 1.0, 10, None, None) == 1
     assert lib.plt_splat_sensor(C.byref(ok), film, C.byref(hits), None, 1.0, 10, None, None) == 6
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_lenses_load_and_match_oracle_paraxials(plt, seed):
+    """The fuzz lenses of tests/test_gpu_fuzz_lenses.py parse in both implementations with
+    the same paraxial matrix, ghost list, and a JIT-compilable all-T program."""
+    from plt_inputs.lenses import random_lens_text
+    text, semi, z_last = random_lens_text(seed)
+    L, O = plt.Lens(text, sensor_z_mm=z_last + 40.0), oracle.load_lens(text, {"sensor_z_mm": z_last + 40.0})
+    for lam in (400.0, 587.5618, 700.0):
+        M = oracle.abcd_vertex_to_vertex(O, lam)
+        assert np.allclose(L.info(lam)["abcd"], M.ravel(), rtol=1e-12, atol=1e-14)
+    ids, _ = L.enumerate_ghosts(2)
+    oids, _ = oracle.enumerate_ghosts(O, 2)
+    assert list(ids) == list(oids)
+    assert L.trace_jit_cubin(L.all_t_id())[:4] == b"\x7fELF"
