@@ -73,3 +73,38 @@ def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, 
             src = dst
         eval_map(m, src, h, stream=stream)
     shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale, n=n, stream=stream)
+
+
+def path_energies(lens, path_ids, rays, direction: int = 0, precision: int = FP64, stream=None, hits=None):
+    """Flux each path carries for the ray batch `rays` (higher-order
+    ghost pruning on the GPU).  Every path is traced and its valid hits are splatted, in
+    the trace kernel, into a ONE-pixel film covering the whole output plane: the film entry
+    is the exact int64 sum of llrint(I * |w_z| * 2^32) over the path's valid rays (Eq. 8
+    with G = |w_z|, weight scale 1), so energies are deterministic and need no extra kernel.
+    Returns a list of floats (sum of I |w_z| per path, same order as path_ids); one
+    device-to-host copy at the end."""
+    import torch
+    from . import alloc_hits
+    dev = rays["ox"].device
+    n = int(rays["ox"].numel())
+    h = hits if hits is not None else alloc_hits(n, device=dev)
+    films = torch.zeros(len(path_ids), dtype=torch.int64, device=dev)
+    whole = {"width_px": 1, "height_px": 1, "channels": 1, "sensor_w_mm": 1e9, "sensor_h_mm": 1e9}
+    for k, pid in enumerate(path_ids):
+        trace_rays(lens, int(pid), rays, h, direction=direction, precision=precision, n=n, stream=stream,
+                   splat={"film_desc": whole, "film": films[k:k + 1], "weight_scale": 1.0})
+    return [float(v) / 4294967296.0 for v in films.cpu().tolist()]
+
+
+def prune_paths(lens, path_ids, rays, min_fraction: float, direction: int = 0, precision: int = FP64,
+                stream=None):
+    """Keep the paths whose measured flux (path_energies) is at least `min_fraction` of the
+    all-transmission path's flux on the same rays -- the GPU counterpart of the host's
+    normal-incidence prune (plt_enumerate_ghosts min_throughput), measured on real rays
+    through real apertures instead of one paraxial ray.  Returns (kept ids, energies dict)."""
+    ids = [int(p) for p in path_ids]
+    all_t = lens.all_t_id()
+    e = path_energies(lens, [all_t] + ids, rays, direction, precision, stream)
+    ref = e[0]
+    energies = dict(zip(ids, e[1:]))
+    return [p for p in ids if ref > 0 and energies[p] >= min_fraction * ref], energies
