@@ -297,6 +297,22 @@ PLT_API plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_m
                                    int64_t pixels, float weight_scale, int64_t* film, int64_t n, void* cuda_stream);
 
 /*
+ * plt_shade_plane with the Monte-Carlo weight of pupil sampling (SURVEY.md §8(f) NEXT-3
+ * remainder).  Eq. 9 integrates L T cos(theta) over the hemisphere at the sensor point;
+ * when ray i's direction was drawn through a uniform point on a disc of area A parallel
+ * to the sensor at axial distance dz (an exit pupil, or the rear clear aperture), its
+ * solid-angle pdf is dz^2 / (A cos^3 theta), so the estimator weight is
+ * (A / dz^2) cos^4 theta.  in_dz (device, n floats) holds the z-components w_z of the
+ * SENSOR rays (cos theta = |w_z|); the caller folds A / dz^2 (and 1/spp) into
+ * weight_scale: film[i / spp] += llrint(I * L * ((w_z^2)^2) * weight_scale * 2^32),
+ * IEEE double in that order (bit-identical to oracle.shade_plane with in_dz).
+ * Errors: PLT_E_INVALID_ARG (also in_dz == NULL), PLT_E_CUDA.
+ */
+PLT_API plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits,
+                                            int spp, int64_t pixels, float weight_scale, const float* in_dz,
+                                            int64_t* film, int64_t n, void* cuda_stream);
+
+/*
  * Free-space propagation to the plane z = z_target_mm (sensor-shift focusing with one
  * precomputed map): o' = o + ((z_t - z_in)/w_z) w in float32 (round-to-nearest,
  * one fma per coordinate), w and lambda copied.  in->plane_z_mm is z_in; out's arrays

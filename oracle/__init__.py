@@ -235,16 +235,19 @@ def splat(film: dict, valid, px, py, dz, I, channel=None, scale: float = 1.0):
 
 
 def shade_plane(scene: dict, z_hits: float, valid, px, py, dx, dy, dz, I, spp: int, pixels: int,
-                scale: float = 1.0):
+                scale: float = 1.0, in_dz=None):
     """O14 (Eq. 9): backward camera integrand on a
-    checkerboard scene plane -> int64 film of `pixels` (film[i // spp])."""
+    checkerboard scene plane -> int64 film of `pixels` (film[i // spp]).  in_dz (optional,
+    the sensor rays' w_z): weight each ray by cos^4(theta), the pupil-sampling estimator
+    weight (include/plt.h plt_shade_plane_weighted)."""
     f = np.zeros(int(pixels), np.int64)
     v = np.ascontiguousarray(valid, dtype=np.uint8)
     a = [np.ascontiguousarray(x, dtype=np.float32) for x in (px, py, dx, dy, dz, I)]
+    w = None if in_dz is None else np.ascontiguousarray(in_dz, dtype=np.float32)
     p = _lib.ptr
     _lib.lib().orc_shade_plane(float(scene["z_mm"]), float(scene["period_mm"]), float(scene["contrast"]),
                                float(z_hits), int(spp), int(pixels), np.float32(scale), p(f), v.size, p(v),
-                               *[p(x) for x in a])
+                               *[p(x) for x in a], p(w) if w is not None else None)
     return f
 
 

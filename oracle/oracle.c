@@ -402,8 +402,12 @@ int64_t orc_splat(int width, int height, int channels, double W, double H, doubl
 /* ------------------------------------------------------------------------- */
 void orc_shade_plane(double z_scene, double period, double contrast, double z_hits, int spp, int64_t pixels,
                      float scale, int64_t* film, int64_t n, const uint8_t* valid, const float* px, const float* py,
-                     const float* dx, const float* dy, const float* dz, const float* I)
+                     const float* dx, const float* dy, const float* dz, const float* I, const float* in_dz)
 {
+    /* in_dz (nullable): z-components of the SENSOR rays; when given, each contribution is
+     * weighted by cos^4(theta) = (w_z^2)^2, the Monte-Carlo weight of directions drawn
+     * through uniform points on a disc parallel to the sensor (Eq. 9 with the pdf
+     * dz^2 / (A cos^3 theta); A / dz^2 is the caller's scale). */
     for (int64_t i = 0; i < n; ++i) {
         if (!valid[i]) continue;
         const double t = (z_scene - z_hits) / (double)dz[i];
@@ -413,6 +417,8 @@ void orc_shade_plane(double z_scene, double period, double contrast, double z_hi
         const double y = (double)py[i] + t * (double)dy[i];
         const int64_t q = (int64_t)floor(x / period) + (int64_t)floor(y / period);
         const double L = (q & 1) ? contrast : 1.0;
-        film[pix] += llrint((double)I[i] * L * (double)scale * 4294967296.0);
+        double IL = (double)I[i] * L;
+        if (in_dz) { const double c = (double)in_dz[i], c2 = c * c; IL = IL * (c2 * c2); }
+        film[pix] += llrint(IL * (double)scale * 4294967296.0);
     }
 }

@@ -268,8 +268,9 @@ plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir d
     PLT_GUARD_END
 }
 
-plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
-                           int64_t pixels, float weight_scale, int64_t* film, int64_t n, void* cuda_stream) {
+static plt_status shade_impl(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
+                             int64_t pixels, float weight_scale, const float* in_dz, int64_t* film, int64_t n,
+                             void* cuda_stream) {
     PLT_GUARD_BEGIN
     if (!scene || !hits || !film) return set_err(PLT_E_INVALID_ARG, "null scene/hits/film");
     if (!(scene->period_mm > 0) || !std::isfinite(scene->z_mm) || !std::isfinite(scene->contrast) ||
@@ -282,9 +283,22 @@ plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const
     plt_status s = check_device();
     if (s != PLT_OK) return s;
     const plt::ScenePlane sc{scene->z_mm, scene->period_mm, scene->contrast};
-    return cuda_status(plt::launch_shade_plane(sc, z_hits_mm, *hits, spp, pixels, weight_scale, film, n, cuda_stream),
+    return cuda_status(plt::launch_shade_plane(sc, z_hits_mm, *hits, spp, pixels, weight_scale, film, n, cuda_stream,
+                                                  in_dz),
                        "shade_plane");
     PLT_GUARD_END
+}
+
+plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
+                           int64_t pixels, float weight_scale, int64_t* film, int64_t n, void* cuda_stream) {
+    return shade_impl(scene, z_hits_mm, hits, spp, pixels, weight_scale, nullptr, film, n, cuda_stream);
+}
+
+plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
+                                    int64_t pixels, float weight_scale, const float* in_dz, int64_t* film, int64_t n,
+                                    void* cuda_stream) {
+    if (!in_dz && n > 0) return set_err(PLT_E_INVALID_ARG, "null in_dz (sensor-ray direction z-components)");
+    return shade_impl(scene, z_hits_mm, hits, spp, pixels, weight_scale, in_dz, film, n, cuda_stream);
 }
 
 plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, int64_t n,

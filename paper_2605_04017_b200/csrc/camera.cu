@@ -20,7 +20,8 @@ namespace {
 constexpr int kThreads = 256;
 
 __global__ void __launch_bounds__(kThreads) shade_plane_kernel(ScenePlane sc, double z_hits, plt_hits hits, int spp,
-                                                               int64_t pixels, float scale, int64_t* film, int64_t n) {
+                                                               int64_t pixels, float scale, int64_t* film, int64_t n,
+                                                               const float* in_dz) {
     __shared__ long long wsm[kThreads];
     const int lane = threadIdx.x & 31, warp0 = threadIdx.x & ~31;
     for (int64_t base = (int64_t)blockIdx.x * kThreads + warp0; base < n; base += (int64_t)gridDim.x * kThreads) {
@@ -35,8 +36,12 @@ __global__ void __launch_bounds__(kThreads) shade_plane_kernel(ScenePlane sc, do
                 const double y = __dadd_rn((double)__ldg(hits.py + i), __dmul_rn(t, (double)__ldg(hits.dy + i)));
                 const long long q = (long long)floor(__ddiv_rn(x, sc.period)) + (long long)floor(__ddiv_rn(y, sc.period));
                 const double L = (q & 1) ? sc.contrast : 1.0;
-                w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn((double)__ldg(hits.throughput + i), L), (double)scale),
-                                             4294967296.0));
+                double IL = __dmul_rn((double)__ldg(hits.throughput + i), L);
+                if (in_dz) {   // pupil-sampling weight cos^4(theta) of the sensor ray (plt_shade_plane_weighted)
+                    const double c = (double)__ldg(in_dz + i), c2 = __dmul_rn(c, c);
+                    IL = __dmul_rn(IL, __dmul_rn(c2, c2));
+                }
+                w = __double2ll_rn(__dmul_rn(__dmul_rn(IL, (double)scale), 4294967296.0));
                 key = pix;
             }
         }
@@ -87,9 +92,9 @@ int blocks_for(int64_t n) {
 }  // namespace
 
 int launch_shade_plane(const ScenePlane& sc, double z_hits, const plt_hits& hits, int spp, int64_t pixels,
-                       float scale, int64_t* film, int64_t n, void* stream) {
+                       float scale, int64_t* film, int64_t n, void* stream, const float* in_dz) {
     shade_plane_kernel<<<blocks_for(n), kThreads, 0, (cudaStream_t)stream>>>(sc, z_hits, hits, spp, pixels, scale,
-                                                                             film, n);
+                                                                             film, n, in_dz);
     return (int)cudaGetLastError();
 }
 

@@ -49,14 +49,18 @@ def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict
 
 
 def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, m=None, map_plane_z: float | None = None,
-               weight_scale: float = 1.0, hits=None, scratch_rays=None, stream=None):
+               weight_scale: float = 1.0, hits=None, scratch_rays=None, stream=None, pupil_disc: tuple | None = None):
     """Backward depth-of-field image (the camera integrator of
     P:422-427, Eq. 9): pixel-stratified sensor rays (e.g. the sensor_grid law, ray i in
     pixel i // spp) go through the lens -- by the exact all-T trace, or by the map `m`
     after free-space propagation to the map's input plane `map_plane_z` (focusing by a
     sensor shift needs no retraining) -- and their exit rays (on z = z_exit_mm,
     the lens's backward exit plane) are shaded on the checkerboard scene plane into `film`
-    (device int64, one entry per pixel, not cleared).
+    (device int64, one entry per pixel, not cleared).  pupil_disc = (z_mm, radius_mm) of
+    the disc the sensor rays' directions were sampled through (e.g. the exit pupil of
+    plt_lens_pupils): each ray then carries the Eq. 9 estimator weight
+    (pi r^2 / dz^2) cos^4(theta) (plt_shade_plane_weighted), making the image an unbiased
+    estimate of the pixel integral rather than of the ray average.
     """
     from . import alloc_hits
     import torch
@@ -72,7 +76,16 @@ def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, 
             propagate_rays(rays, dst, map_plane_z, stream=stream)
             src = dst
         eval_map(m, src, h, stream=stream)
-    shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale, n=n, stream=stream)
+    if pupil_disc is None:
+        shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale, n=n, stream=stream)
+    else:
+        if rays.get("dz") is None:
+            raise ValueError("pupil weighting needs the sensor rays' dz")
+        import math
+        z_disc, r_disc = float(pupil_disc[0]), float(pupil_disc[1])
+        dz = abs(float(rays["plane_z"]) - z_disc)
+        shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale * math.pi * r_disc ** 2 / dz ** 2, n=n,
+                    stream=stream, in_dz=rays["dz"])
 
 
 def path_energies(lens, path_ids, rays, direction: int = 0, precision: int = FP64, stream=None, hits=None):

@@ -37,6 +37,16 @@ def test_shade_plane_bit_exact_on_trace_hits(gpu_lib, spp):
                              hh["dz"], hh["throughput"], spp=spp, pixels=pixels, scale=0.5)
     assert valid.mean() > 0.02
     assert np.array_equal(film.cpu().numpy(), ref)
+    # the pupil-sampling weighted form (cos^4 of the sensor rays), bit-exact as well
+    fw = torch.zeros(pixels, dtype=torch.int64, device="cuda")
+    plt.shade_plane(SCENE, cfg["opts"]["backward_exit_z_mm"], h, fw, spp, pixels=pixels, weight_scale=0.5,
+                    in_dz=d["dz"])
+    torch.cuda.synchronize()
+    refw = oracle.shade_plane(SCENE, cfg["opts"]["backward_exit_z_mm"], valid, hh["px"], hh["py"], hh["dx"],
+                              hh["dy"], hh["dz"], hh["throughput"], spp=spp, pixels=pixels, scale=0.5,
+                              in_dz=d["dz"].cpu().numpy())
+    assert np.array_equal(fw.cpu().numpy(), refw)
+    assert 0 < refw.sum() < ref.sum()
 
 
 def test_propagate_matches_closed_form(gpu_lib):
@@ -112,3 +122,37 @@ def test_exit_pupil_sampling_raises_the_valid_fraction(gpu_lib):
         fr[key] = float(unpack_mask(h["mask_bits"].cpu().numpy(), n).mean())
     print(fr)
     assert fr["exit"] > 5 * fr["rear"] and fr["exit"] > 0.5
+
+
+def test_pupil_weights_make_sampling_strategies_agree(gpu_lib):
+    """With the Eq. 9 pupil-sampling weights (render_dof(pupil_disc=...)), rays aimed at the
+    rear clear aperture and rays aimed at 1.2x the paraxial exit pupil estimate the SAME
+    image (the pixel integral), although their ray averages differ several-fold."""
+    import torch
+    from paper_2605_04017_b200.render import render_dof
+    plt = gpu_lib
+    cfg = C.CONFIGS["C3_DOF"]
+    lens = plt.Lens(C.lens_text("C3_DOF"), **cfg["opts"])
+    pp = lens.pupils()
+    law0 = C.dof_law(0.0, 64)
+    px = cfg["width_px"] * cfg["height_px"]
+    imgs = {}
+    for key, disc in (("rear", (law0["pupil_z"], law0["pupil_r"])),
+                      ("exit", (pp["exit_z_mm"], 1.2 * pp["exit_r_mm"]))):
+        n = px * 64
+        d = plt.rays_to_device(R.gen_rays(C.dof_law(0.0, 64, disc), cfg["seed"], 0, n))
+        fw, fu = (torch.zeros(px, dtype=torch.int64, device="cuda") for _ in range(2))
+        render_dof(lens, d, cfg["scene"], fw, 64, cfg["opts"]["backward_exit_z_mm"], weight_scale=1.0 / 64,
+                   pupil_disc=disc)
+        render_dof(lens, d, cfg["scene"], fu, 64, cfg["opts"]["backward_exit_z_mm"], weight_scale=1.0 / 64)
+        torch.cuda.synchronize()
+        imgs[key] = (fw.cpu().numpy().astype(np.float64), fu.cpu().numpy().astype(np.float64))
+    (wr, ur), (we, ue) = imgs["rear"], imgs["exit"]
+    ratio_w, ratio_u = we.sum() / wr.sum(), ue.sum() / ur.sum()
+    # 16x16-pixel bins: the weighted images agree to Monte-Carlo noise (the rear-aperture
+    # rays are only ~7 % valid: ~1,200 valid rays per bin)
+    b = lambda f: f.reshape(cfg["height_px"] // 16, 16, cfg["width_px"] // 16, 16).sum((1, 3))
+    rel = np.abs(b(we) - b(wr)).sum() / b(wr).sum()
+    print({"weighted_energy_ratio": ratio_w, "unweighted_energy_ratio": ratio_u, "rel_l1_bin16": rel})
+    assert abs(ratio_w - 1.0) < 0.03 and abs(ratio_u - 1.0) > 0.5
+    assert rel < 0.05

@@ -54,3 +54,28 @@ def test_propagation_stays_on_the_ray_and_reaches_the_plane():
     # (o' - o) is parallel to w and its z step is exactly the plane distance
     step = np.stack([p["ox"] - rays["ox"], p["oy"] - rays["oy"], np.full(n, -2.0)], 1)
     assert np.allclose(np.cross(step, w), 0.0, atol=1e-12)
+
+
+def test_pupil_sampling_weight_reproduces_the_projected_solid_angle():
+    """Eq. 9 with directions drawn through uniform points on a disc (radius r, axial
+    distance D) parallel to the sensor: weighting each ray by (A / D^2) cos^4(theta)
+    estimates the cosine-weighted solid angle of the disc seen from the on-axis sensor
+    point, pi sin^2(alpha) with tan(alpha) = r / D (closed form).  A cos^3 or cos^5 weight
+    misses it by several percent."""
+    r, D, m = 6.0, 12.0, 1 << 18
+    k = np.arange(m)
+    rad = r * np.sqrt((k + 0.5) / m)                        # stratified radius x golden-angle
+    phi = k * np.pi * (3.0 - np.sqrt(5.0))
+    px, py = rad * np.cos(phi), rad * np.sin(phi)
+    w = np.stack([px, py, np.full(m, D)], 1)
+    w /= np.linalg.norm(w, axis=1, keepdims=True)
+    ones, zeros = np.ones(m, np.float32), np.zeros(m, np.float32)
+    scene = {"z_mm": -100.0, "period_mm": 1e6, "contrast": 1.0}     # uniform radiance L = 1
+    A = np.pi * r * r
+    f = oracle.shade_plane(scene, 0.0, np.ones(m, bool), zeros, zeros, zeros, zeros, -ones, ones, spp=m, pixels=1,
+                           scale=A / D ** 2 / m, in_dz=w[:, 2].astype(np.float32))
+    est = f[0] / 2.0 ** 32
+    sin2 = r * r / (r * r + D * D)
+    assert abs(est - np.pi * sin2) < 2e-3 * np.pi * sin2
+    cos3 = np.mean(w[:, 2] ** 3) * A / D ** 2
+    assert abs(cos3 - np.pi * sin2) > 0.03 * np.pi * sin2
