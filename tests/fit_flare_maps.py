@@ -91,6 +91,10 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "maps", "flare"))
     ap.add_argument("--report", default=None)
     ap.add_argument("--max-paths", type=int, default=0, help="debug: only the first k ghosts")
+    ap.add_argument("--only", default="", help="comma-separated path ids to fit (others untouched)")
+    ap.add_argument("--mcmc", type=int, default=0,
+                    help="paths with fewer than --min-valid uniform valid rays get this many extra valid "
+                         "training rays from the valid-region MCMC sampler (P:385; tests/mcmc_valid.py)")
     a = ap.parse_args()
     torch.manual_seed(0)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
@@ -101,11 +105,33 @@ def main():
     ids = [int(i) for i in all_ids if int(i) != oracle.all_t_id(olens.n_optical)]
     if a.max_paths:
         ids = ids[:a.max_paths]
+    if a.only:
+        want = {int(x) for x in a.only.split(",")}
+        ids = [i for i in ids if i in want]
+    if a.mcmc and not a.only:
+        ap.error("--mcmc is meant for the low-valid paths: list them with --only (equal sample counts)")
     t0 = time.time()
     xs, ys, vs, keep = [], [], [], []
     for k, pid in enumerate(ids):
         inp, out, valid = oracle_labels(olens, pid, cfg["direction"], law, 8_000_000 + k, a.rays, "cpu")
         nv = int(valid.sum())
+        if nv < a.min_valid and a.mcmc:
+            from fit_map import RAY_KEYS
+            from mcmc_valid import sample_valid, to_rays
+            try:
+                st = sample_valid(olens, pid, cfg["direction"], law, law["lam"], a.mcmc, seed=9_000_000 + k,
+                                  threads=oracle.host_threads())
+            except RuntimeError as e:
+                print(e, flush=True)
+                st = None
+            if st is not None:
+                mr = to_rays(st, law)
+                o = oracle.trace(olens, pid, cfg["direction"], mr, threads=oracle.host_threads())
+                inp = torch.cat([inp, torch.from_numpy(np.stack([mr[kk] for kk in RAY_KEYS], 1))])
+                out = torch.cat([out, torch.from_numpy(np.stack([o[kk] for kk in ("px", "py", "dx", "dy", "dz", "I")], 1))])
+                valid = torch.cat([valid, torch.from_numpy(o["valid"])])
+                print(f"path {pid}: {nv} uniform valid rays + {int(o['valid'].sum())} from MCMC", flush=True)
+                nv = int(valid.sum())
         if nv < a.min_valid:
             print(f"path {pid}: {nv} valid training rays -> no map", flush=True)
             continue
@@ -113,6 +139,9 @@ def main():
         xs.append(x); ys.append(y); vs.append(valid); keep.append(pid)
     P = len(keep)
     print(f"labels for {len(ids)} paths ({P} fitted) in {time.time() - t0:.1f} s", flush=True)
+    if P == 0:
+        print("no path has enough valid rays to fit", flush=True)
+        return
 
     # per-path normalisation (as fit_map): inputs to [-1, 1] with a 1 % margin, outputs (mid, half)
     lo = torch.stack([x.min(0).values for x in xs]); hi = torch.stack([x.max(0).values for x in xs])

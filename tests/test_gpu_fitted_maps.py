@@ -100,10 +100,11 @@ def test_fitted_ghost_map_flare_film(gpu_lib, path):
 
 
 FLARE_MAPS = sorted(glob.glob(os.path.join(ROOT, "maps", "flare", "*", "*.pltmap")))
+MCMC_MAPS = [os.path.join(ROOT, "maps", "flare", "C4_59", "16810240.pltmap")]   # trained on MCMC samples
 
 
-@pytest.mark.parametrize("path", MAPS + FLARE_MAPS[::12],
-                         ids=[os.path.relpath(p, os.path.join(ROOT, "maps")) for p in MAPS + FLARE_MAPS[::12]])
+@pytest.mark.parametrize("path", MAPS + FLARE_MAPS[::12] + MCMC_MAPS,
+                         ids=[os.path.relpath(p, os.path.join(ROOT, "maps")) for p in MAPS + FLARE_MAPS[::12] + MCMC_MAPS])
 def test_fitted_map_kernel_parity(gpu_lib, path):
     """PARITY of the eval_map kernel on trained weights (the bench's map and the flare
     maps) against the float64 oracle's O10 on the same blob: raw logit and regressor
