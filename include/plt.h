@@ -313,6 +313,27 @@ PLT_API plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double
                                             int64_t* film, int64_t n, void* cuda_stream);
 
 /*
+ * Scene of several checkerboard cards at different depths (scenes
+ * beyond one plane -- a depth-of-field target whose cards come into focus at different
+ * sensor shifts).  Card k: plane z = z_mm (object side), axis-aligned rectangle
+ * [x0_mm, x1_mm] x [y0_mm, y1_mm], checker period and odd-square contrast as
+ * plt_scene_plane.  A valid backward exit ray takes the radiance of the card it meets
+ * first -- smallest t = (z_k - z_hits)/w_z > 0 whose hit point lies inside the rectangle
+ * (ties: lower k) -- or `background` if it meets none.  Weighting as
+ * plt_shade_plane_weighted when in_dz != NULL, else as plt_shade_plane.  IEEE double,
+ * exact int64 sum (bit-identical to oracle.shade_cards).  1 <= n_cards <= 8.
+ * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ */
+typedef struct {
+    double z_mm, period_mm, contrast;
+    double x0_mm, x1_mm, y0_mm, y1_mm;
+} plt_scene_card;
+
+PLT_API plt_status plt_shade_cards(const plt_scene_card* cards, int n_cards, double background, double z_hits_mm,
+                                   const plt_hits* hits, int spp, int64_t pixels, float weight_scale,
+                                   const float* in_dz, int64_t* film, int64_t n, void* cuda_stream);
+
+/*
  * Free-space propagation to the plane z = z_target_mm (sensor-shift focusing with one
  * precomputed map): o' = o + ((z_t - z_in)/w_z) w in float32 (round-to-nearest,
  * one fma per coordinate), w and lambda copied.  in->plane_z_mm is z_in; out's arrays

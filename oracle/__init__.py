@@ -251,6 +251,24 @@ def shade_plane(scene: dict, z_hits: float, valid, px, py, dx, dy, dz, I, spp: i
     return f
 
 
+def shade_cards(cards: list, background: float, z_hits: float, valid, px, py, dx, dy, dz, I, spp: int, pixels: int,
+                scale: float = 1.0, in_dz=None):
+    """O14b: several checkerboard cards (dicts z_mm, period_mm, contrast, x0_mm, x1_mm,
+    y0_mm, y1_mm); each valid ray takes the first card it meets inside its rectangle,
+    else `background` (include/plt.h plt_shade_cards)."""
+    f = np.zeros(int(pixels), np.int64)
+    v = np.ascontiguousarray(valid, dtype=np.uint8)
+    a = [np.ascontiguousarray(x, dtype=np.float32) for x in (px, py, dx, dy, dz, I)]
+    w = None if in_dz is None else np.ascontiguousarray(in_dz, dtype=np.float32)
+    cd = np.ascontiguousarray([[c["z_mm"], c["period_mm"], c["contrast"], c["x0_mm"], c["x1_mm"], c["y0_mm"],
+                                c["y1_mm"]] for c in cards], dtype=np.float64)
+    p = _lib.ptr
+    _lib.lib().orc_shade_cards(p(cd), len(cards), float(background), float(z_hits), int(spp), int(pixels),
+                               np.float32(scale), p(f), v.size, p(v), *[p(x) for x in a],
+                               p(w) if w is not None else None)
+    return f
+
+
 def propagate(rays: dict, z_target: float) -> dict:
     """Free-space propagation to z = z_target in float64 (closed form o + ((z_t - z_0)/w_z) w)."""
     towards = 1.0 if float(z_target) >= float(rays["plane_z"]) else -1.0

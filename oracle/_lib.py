@@ -43,6 +43,8 @@ def lib():
         L.orc_splat.argtypes = [i, i, i, d, d, d, d, p, i64, p, p, p, p, p, p, C.c_float]
         L.orc_shade_plane.restype = None
         L.orc_shade_plane.argtypes = [d, d, d, d, i, i64, C.c_float, p, i64, p, p, p, p, p, p, p, p]
+        L.orc_shade_cards.restype = None
+        L.orc_shade_cards.argtypes = [p, i, d, d, i, i64, C.c_float, p, i64, p, p, p, p, p, p, p, p]
         _lib = L
     return _lib
 

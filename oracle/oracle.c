@@ -422,3 +422,38 @@ void orc_shade_plane(double z_scene, double period, double contrast, double z_hi
         film[pix] += llrint(IL * (double)scale * 4294967296.0);
     }
 }
+
+/* ------------------------------------------------------------------------- */
+/* O14b scene cards (scenes beyond one plane): the ray     */
+/* takes the radiance of the first card it meets -- smallest t = (z_k - z_hits) */
+/* / w_z > 0 with the hit inside the card's rectangle (ties: lower k) -- else   */
+/* `background`; cards[7k..7k+6] = z, period, contrast, x0, x1, y0, y1.  The    */
+/* pupil weight as orc_shade_plane.                                            */
+/* ------------------------------------------------------------------------- */
+void orc_shade_cards(const double* cards, int n_cards, double background, double z_hits, int spp, int64_t pixels,
+                     float scale, int64_t* film, int64_t n, const uint8_t* valid, const float* px, const float* py,
+                     const float* dx, const float* dy, const float* dz, const float* I, const float* in_dz)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        if (!valid[i]) continue;
+        const int64_t pix = i / spp;
+        if (pix >= pixels) continue;
+        double L = background, best = 0.0;
+        int found = 0;
+        for (int k = 0; k < n_cards; ++k) {
+            const double* c = cards + 7 * k;
+            const double t = (c[0] - z_hits) / (double)dz[i];
+            if (!(t > 0.0) || (found && !(t < best))) continue;
+            const double x = (double)px[i] + t * (double)dx[i];
+            const double y = (double)py[i] + t * (double)dy[i];
+            if (x < c[3] || x > c[4] || y < c[5] || y > c[6]) continue;
+            const int64_t q = (int64_t)floor(x / c[1]) + (int64_t)floor(y / c[1]);
+            L = (q & 1) ? c[2] : 1.0;
+            best = t;
+            found = 1;
+        }
+        double IL = (double)I[i] * L;
+        if (in_dz) { const double cz = (double)in_dz[i], c2 = cz * cz; IL = IL * (c2 * c2); }
+        film[pix] += llrint(IL * (double)scale * 4294967296.0);
+    }
+}

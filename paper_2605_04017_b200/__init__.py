@@ -29,8 +29,8 @@ _STATUS = {0: "PLT_OK", 1: "PLT_E_INVALID_ARG", 2: "PLT_E_PARSE", 3: "PLT_E_VALI
 EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "plt_lens_info",
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
-            "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_propagate_rays",
-            "plt_lens_pupils")
+            "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_shade_cards",
+            "plt_propagate_rays", "plt_lens_pupils")
 
 
 class PltError(RuntimeError):
@@ -102,12 +102,13 @@ def load():
     L.plt_trace_jit_cubin.argtypes = [p, u64, i, p, C.c_size_t, C.POINTER(C.c_size_t)]
     L.plt_shade_plane.argtypes = [p, d, p, i, i64, C.c_float, p, i64, p]
     L.plt_shade_plane_weighted.argtypes = [p, d, p, i, i64, C.c_float, p, p, i64, p]
+    L.plt_shade_cards.argtypes = [p, i, d, d, p, i, i64, C.c_float, p, p, i64, p]
     L.plt_propagate_rays.argtypes = [p, p, d, i64, p]
     L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
               "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted",
-              "plt_propagate_rays", "plt_lens_pupils"):
+              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -356,6 +357,26 @@ def shade_plane(scene: dict, z_hits_mm: float, hits: dict, film, spp: int, pixel
         _check(load().plt_shade_plane_weighted(C.byref(sc), float(z_hits_mm), C.byref(h), int(spp), pixels,
                                                float(weight_scale), _ptr(in_dz, n, torch.float32),
                                                _ptr(film, pixels, torch.int64), n, _stream(stream)))
+
+
+class SceneCard(C.Structure):
+    _fields_ = [("z_mm", C.c_double), ("period_mm", C.c_double), ("contrast", C.c_double), ("x0_mm", C.c_double),
+                ("x1_mm", C.c_double), ("y0_mm", C.c_double), ("y1_mm", C.c_double)]
+
+
+def shade_cards(cards: list, background: float, z_hits_mm: float, hits: dict, film, spp: int,
+                pixels: int | None = None, weight_scale: float = 1.0, n: int | None = None, stream=None, in_dz=None):
+    """plt_shade_cards: backward camera integrand on a scene of several checkerboard cards
+    (dicts z_mm, period_mm, contrast, x0_mm, x1_mm, y0_mm, y1_mm); in_dz as shade_plane."""
+    import torch
+    n = int(hits["px"].numel()) if n is None else int(n)
+    pixels = int(film.numel()) if pixels is None else int(pixels)
+    arr = (SceneCard * len(cards))(*[SceneCard(c["z_mm"], c["period_mm"], c["contrast"], c["x0_mm"], c["x1_mm"],
+                                               c["y0_mm"], c["y1_mm"]) for c in cards])
+    h = _hits_struct(hits, n)
+    _check(load().plt_shade_cards(arr, len(cards), float(background), float(z_hits_mm), C.byref(h), int(spp), pixels,
+                                  float(weight_scale), _ptr(in_dz, n, torch.float32) if in_dz is not None else None,
+                                  _ptr(film, pixels, torch.int64), n, _stream(stream)))
 
 
 def propagate_rays(rays: dict, out: dict, z_target_mm: float, n: int | None = None, stream=None):

@@ -294,6 +294,36 @@ plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const
     return shade_impl(scene, z_hits_mm, hits, spp, pixels, weight_scale, nullptr, film, n, cuda_stream);
 }
 
+plt_status plt_shade_cards(const plt_scene_card* cards, int n_cards, double background, double z_hits_mm,
+                           const plt_hits* hits, int spp, int64_t pixels, float weight_scale, const float* in_dz,
+                           int64_t* film, int64_t n, void* cuda_stream) {
+    PLT_GUARD_BEGIN
+    if (!cards || !hits || !film) return set_err(PLT_E_INVALID_ARG, "null cards/hits/film");
+    if (n_cards < 1 || n_cards > plt::kMaxCards) return set_err(PLT_E_INVALID_ARG, "n_cards must be 1..8");
+    plt::SceneCards sc{};
+    sc.n = n_cards;
+    sc.background = background;
+    for (int k = 0; k < n_cards; ++k) {
+        const plt_scene_card& c = cards[k];
+        if (!(c.period_mm > 0) || !std::isfinite(c.z_mm) || !std::isfinite(c.contrast) || !(c.x1_mm >= c.x0_mm) ||
+            !(c.y1_mm >= c.y0_mm))
+            return set_err(PLT_E_INVALID_ARG, "bad scene card " + std::to_string(k));
+        sc.z[k] = c.z_mm; sc.period[k] = c.period_mm; sc.contrast[k] = c.contrast;
+        sc.x0[k] = c.x0_mm; sc.x1[k] = c.x1_mm; sc.y0[k] = c.y0_mm; sc.y1[k] = c.y1_mm;
+    }
+    if (!std::isfinite(background) || !std::isfinite(z_hits_mm)) return set_err(PLT_E_INVALID_ARG, "bad scene");
+    if (spp <= 0 || pixels <= 0 || n < 0) return set_err(PLT_E_INVALID_ARG, "spp, pixels must be > 0 and n >= 0");
+    if (n == 0) return PLT_OK;
+    if (!hits->mask_bits || !hits->px || !hits->py || !hits->dx || !hits->dy || !hits->dz || !hits->throughput)
+        return set_err(PLT_E_INVALID_ARG, "null hit arrays");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    return cuda_status(plt::launch_shade_cards(sc, z_hits_mm, *hits, spp, pixels, weight_scale, film, n, cuda_stream,
+                                               in_dz),
+                       "shade_cards");
+    PLT_GUARD_END
+}
+
 plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
                                     int64_t pixels, float weight_scale, const float* in_dz, int64_t* film, int64_t n,
                                     void* cuda_stream) {

@@ -57,6 +57,55 @@ __global__ void __launch_bounds__(kThreads) shade_plane_kernel(ScenePlane sc, do
     }
 }
 
+// Several cards (plt_shade_cards): the nearest card whose rectangle contains the hit.
+__global__ void __launch_bounds__(kThreads) shade_cards_kernel(const __grid_constant__ SceneCards sc, double z_hits,
+                                                               plt_hits hits, int spp, int64_t pixels, float scale,
+                                                               int64_t* film, int64_t n, const float* in_dz) {
+    __shared__ long long wsm[kThreads];
+    const int lane = threadIdx.x & 31, warp0 = threadIdx.x & ~31;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads + warp0; base < n; base += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = base + lane;
+        long long key = -1, w = 0;
+        if (i < n && ((__ldg(hits.mask_bits + (i >> 5)) >> (i & 31)) & 1u)) {
+            const int64_t pix = i / spp;
+            if (pix < pixels) {
+                const double dz = (double)__ldg(hits.dz + i), px = (double)__ldg(hits.px + i),
+                             py = (double)__ldg(hits.py + i), dx = (double)__ldg(hits.dx + i),
+                             dy = (double)__ldg(hits.dy + i);
+                double L = sc.background, best = 0.0;
+                bool found = false;
+                for (int k = 0; k < sc.n; ++k) {
+                    const double t = __ddiv_rn(__dsub_rn(sc.z[k], z_hits), dz);
+                    if (!(t > 0.0) || (found && !(t < best))) continue;
+                    const double x = __dadd_rn(px, __dmul_rn(t, dx)), y = __dadd_rn(py, __dmul_rn(t, dy));
+                    if (x < sc.x0[k] || x > sc.x1[k] || y < sc.y0[k] || y > sc.y1[k]) continue;
+                    const long long q = (long long)floor(__ddiv_rn(x, sc.period[k])) +
+                                        (long long)floor(__ddiv_rn(y, sc.period[k]));
+                    L = (q & 1) ? sc.contrast[k] : 1.0;
+                    best = t;
+                    found = true;
+                }
+                double IL = __dmul_rn((double)__ldg(hits.throughput + i), L);
+                if (in_dz) {
+                    const double c = (double)__ldg(in_dz + i), c2 = __dmul_rn(c, c);
+                    IL = __dmul_rn(IL, __dmul_rn(c2, c2));
+                }
+                w = __double2ll_rn(__dmul_rn(__dmul_rn(IL, (double)scale), 4294967296.0));
+                key = pix;
+            }
+        }
+        wsm[threadIdx.x] = w;
+        __syncwarp();
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(peers) - 1) {
+            long long sum = 0;
+            for (unsigned p = peers; p; p &= p - 1) sum += wsm[warp0 + __ffs(p) - 1];
+            atomicAdd(reinterpret_cast<unsigned long long*>(film + key), (unsigned long long)sum);
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) propagate_kernel(plt_rays in, plt_rays out, float z_target, int64_t n) {
     const float z0 = (float)in.plane_z_mm;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
@@ -94,6 +143,13 @@ int blocks_for(int64_t n) {
 int launch_shade_plane(const ScenePlane& sc, double z_hits, const plt_hits& hits, int spp, int64_t pixels,
                        float scale, int64_t* film, int64_t n, void* stream, const float* in_dz) {
     shade_plane_kernel<<<blocks_for(n), kThreads, 0, (cudaStream_t)stream>>>(sc, z_hits, hits, spp, pixels, scale,
+                                                                             film, n, in_dz);
+    return (int)cudaGetLastError();
+}
+
+int launch_shade_cards(const SceneCards& sc, double z_hits, const plt_hits& hits, int spp, int64_t pixels,
+                       float scale, int64_t* film, int64_t n, void* stream, const float* in_dz) {
+    shade_cards_kernel<<<blocks_for(n), kThreads, 0, (cudaStream_t)stream>>>(sc, z_hits, hits, spp, pixels, scale,
                                                                              film, n, in_dz);
     return (int)cudaGetLastError();
 }

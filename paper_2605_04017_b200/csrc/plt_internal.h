@@ -137,6 +137,15 @@ std::string trace_jit_cubin(const Program<float>& P, std::string* log_out);
 struct ScenePlane { double z, period, contrast; };
 int launch_shade_plane(const ScenePlane& sc, double z_hits, const plt_hits& hits, int spp, int64_t pixels,
                        float scale, int64_t* film, int64_t n, void* stream, const float* in_dz = nullptr);
+constexpr int kMaxCards = 8;
+struct SceneCards {
+    int n;
+    double background;
+    double z[kMaxCards], period[kMaxCards], contrast[kMaxCards];
+    double x0[kMaxCards], x1[kMaxCards], y0[kMaxCards], y1[kMaxCards];
+};
+int launch_shade_cards(const SceneCards& sc, double z_hits, const plt_hits& hits, int spp, int64_t pixels,
+                       float scale, int64_t* film, int64_t n, void* stream, const float* in_dz);
 int launch_propagate(const plt_rays& in, const plt_rays& out, float z_target, int64_t n, void* stream);
 int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
                  float scale, int64_t n, unsigned long long* dropped, void* stream);

@@ -76,16 +76,21 @@ def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, 
             propagate_rays(rays, dst, map_plane_z, stream=stream)
             src = dst
         eval_map(m, src, h, stream=stream)
-    if pupil_disc is None:
-        shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale, n=n, stream=stream)
-    else:
+    in_dz = None
+    if pupil_disc is not None:
         if rays.get("dz") is None:
             raise ValueError("pupil weighting needs the sensor rays' dz")
         import math
         z_disc, r_disc = float(pupil_disc[0]), float(pupil_disc[1])
         dz = abs(float(rays["plane_z"]) - z_disc)
-        shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale * math.pi * r_disc ** 2 / dz ** 2, n=n,
-                    stream=stream, in_dz=rays["dz"])
+        weight_scale = weight_scale * math.pi * r_disc ** 2 / dz ** 2
+        in_dz = rays["dz"]
+    if "cards" in scene:   # several cards at different depths (plt_shade_cards)
+        from . import shade_cards
+        shade_cards(scene["cards"], scene.get("background", 0.0), z_exit_mm, h, film, spp, weight_scale=weight_scale,
+                    n=n, stream=stream, in_dz=in_dz)
+    else:
+        shade_plane(scene, z_exit_mm, h, film, spp, weight_scale=weight_scale, n=n, stream=stream, in_dz=in_dz)
 
 
 def path_energies(lens, path_ids, rays, direction: int = 0, precision: int = FP64, stream=None, hits=None):

@@ -79,3 +79,40 @@ def test_pupil_sampling_weight_reproduces_the_projected_solid_angle():
     assert abs(est - np.pi * sin2) < 2e-3 * np.pi * sin2
     cos3 = np.mean(w[:, 2] ** 3) * A / D ** 2
     assert abs(cos3 - np.pi * sin2) > 0.03 * np.pi * sin2
+
+
+def test_scene_cards_nearest_card_inside_its_rectangle():
+    """O14b: straight-back rays (w = (0, 0, -1)) from z_hits = 0 through a near card
+    (z = -100, |x| <= 10, y in [-5, 5], uniform L = 1) in front of a far card (z = -500,
+    |x|, |y| <= 40, contrast 0.25 on every square: period huge, so x >= 0 squares are
+    even (L = 1) and x < 0 odd); outside both: background 0.5.  Also: a single card
+    covering the whole plane reproduces shade_plane bit for bit."""
+    near = {"z_mm": -100.0, "period_mm": 1e9, "contrast": 1.0, "x0_mm": -10.0, "x1_mm": 10.0, "y0_mm": -5.0,
+            "y1_mm": 5.0}
+    far = {"z_mm": -500.0, "period_mm": 1e9, "contrast": 0.25, "x0_mm": -40.0, "x1_mm": 40.0, "y0_mm": -40.0,
+           "y1_mm": 40.0}
+    xs = np.array([0.0, 5.0, -20.0, 20.0, 0.0, 60.0, -30.0], np.float32)
+    ys = np.array([0.0, 4.0, 0.0, 0.0, 20.0, 0.0, -50.0], np.float32)
+    n = xs.size
+    ones, zeros = np.ones(n, np.float32), np.zeros(n, np.float32)
+    f = oracle.shade_cards([far, near], 0.5, 0.0, np.ones(n, bool), xs, ys, zeros, zeros, -ones, ones, spp=1,
+                           pixels=n)
+    L = f / 2.0 ** 32
+    # x = -20 hits the far card at x < 0: floor(-20/1e9) = -1 -> odd -> contrast 0.25
+    assert np.allclose(L, [1.0, 1.0, 0.25, 1.0, 1.0, 0.5, 0.5]), L
+    # card order does not matter (nearest wins), single all-covering card == shade_plane
+    assert np.array_equal(f, oracle.shade_cards([near, far], 0.5, 0.0, np.ones(n, bool), xs, ys, zeros, zeros,
+                                                -ones, ones, spp=1, pixels=n))
+    rng = np.random.default_rng(1)
+    m = 4096
+    px, py = rng.uniform(-30, 30, m).astype(np.float32), rng.uniform(-30, 30, m).astype(np.float32)
+    dx, dy = rng.uniform(-0.2, 0.2, m).astype(np.float32), rng.uniform(-0.2, 0.2, m).astype(np.float32)
+    dz = -np.sqrt(1 - dx.astype(np.float64) ** 2 - dy.astype(np.float64) ** 2).astype(np.float32)
+    I = rng.uniform(0.5, 1.0, m).astype(np.float32)
+    val = rng.random(m) < 0.8
+    scene = {"z_mm": -300.0, "period_mm": 7.0, "contrast": 0.3}
+    whole = {"z_mm": -300.0, "period_mm": 7.0, "contrast": 0.3, "x0_mm": -1e9, "x1_mm": 1e9, "y0_mm": -1e9,
+             "y1_mm": 1e9}
+    a = oracle.shade_plane(scene, 0.0, val, px, py, dx, dy, dz, I, spp=4, pixels=m // 4, scale=0.5)
+    b = oracle.shade_cards([whole], 0.0, 0.0, val, px, py, dx, dy, dz, I, spp=4, pixels=m // 4, scale=0.5)
+    assert np.array_equal(a, b)
