@@ -53,13 +53,22 @@ __device__ __forceinline__ void splat_warp(const SplatCtx& c, long long* wsm, bo
     long long w = 0;
     bool drop = false;
     if (hit) key = splat_key(c, px, py, dz, I, ch, w, drop);
-    wsm[lane] = w;
-    __syncwarp();
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (key >= 0 && lane == __ffs(peers) - 1) {
-        long long sum = 0;
-        for (unsigned p = peers; p; p &= p - 1) sum += wsm[__ffs(p) - 1];
-        atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)sum);
+    // Aggregate only where it pays: if no two neighbouring lanes share a pixel (a spread-out
+    // image: the warp's hits almost surely land on 32 distinct pixels) every lane adds its
+    // own weight; otherwise (a bright spot) lanes with the same pixel are grouped with
+    // __match_any_sync and summed first.  Integer adds: the film is the same either way.
+    const int nb = __shfl_down_sync(0xffffffffu, key, 1);
+    if (!__any_sync(0xffffffffu, lane < 31 && key >= 0 && key == nb)) {
+        if (key >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)w);
+    } else {
+        wsm[lane] = w;
+        __syncwarp();
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(peers) - 1) {
+            long long sum = 0;
+            for (unsigned p = peers; p; p &= p - 1) sum += wsm[__ffs(p) - 1];
+            atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)sum);
+        }
     }
     const unsigned dm = __ballot_sync(0xffffffffu, drop);
     if (c.dropped && lane == 0 && dm) atomicAdd(c.dropped, (unsigned long long)__popc(dm));
