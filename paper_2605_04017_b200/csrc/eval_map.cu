@@ -203,8 +203,8 @@ __device__ __forceinline__ float2 tanh_ex2_newton2(float2 x) {
     for (int it = 0; it < 3; ++it) r = __fmul2_rn(r, __ffma2_rn(nd, r, two));
     return __ffma2_rn(make_float2(-2.f, -2.f), r, one);
 }
-#ifndef PLT_MAP_CLS_ACCURATE_HALVES
-#define PLT_MAP_CLS_ACCURATE_HALVES 1   // halves (16 units) of the classifier h1 with the accurate tanh
+#ifndef PLT_MAP_CLS_ACCURATE_UNITS
+#define PLT_MAP_CLS_ACCURATE_UNITS 16   // most logit-influential classifier h1 units with the accurate tanh
 #endif
 #ifndef PLT_MAP_CLS_TANH
 #define PLT_MAP_CLS_TANH 1   // classifier first hidden layer: 0 MUFU tanh, 1 ex2+rcp, 2 rational
@@ -498,10 +498,11 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             tmem_ld16(tmem_row + 16 * half, v);
             PLT_CLK(h1);
             // the classifier's h1 units are ordered by influence on the logit (map.cpp):
-            // the first PLT_MAP_CLS_ACCURATE_HALVES x 16 take the accurate tanh
-            if (accurate && PLT_MAP_CLS_TANH == 1 && half < PLT_MAP_CLS_ACCURATE_HALVES) {
+            // the first PLT_MAP_CLS_ACCURATE_UNITS take the accurate tanh
+            if (accurate && PLT_MAP_CLS_TANH == 1 && 16 * half < PLT_MAP_CLS_ACCURATE_UNITS) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = tanh_accurate(v[j]);
+                for (int j = 0; j < 16; ++j)
+                    v[j] = 16 * half + j < PLT_MAP_CLS_ACCURATE_UNITS ? tanh_accurate(v[j]) : tanh_approx(v[j]);
             } else if (accurate && PLT_MAP_CLS_TANH == 3) {
 #pragma unroll
                 for (int j = 0; j < 16; j += 2) {
