@@ -58,6 +58,6 @@ def test_rays_missing_the_lens_and_axial_rays(gpu_lib):
     for prec in (0, 1):
         g = gpu_trace(plt, gl, gl.all_t_id(), rays, precision=prec)
         o = oracle.trace(ol, gl.all_t_id(), 0, rays)
-        compare_trace(g, o)
+        compare_trace(g, o, excluded_max=32)           # the 32 grazing rays have |w_z| = 0
         assert not g["valid"][:32].any() and g["valid"][32:64].all() and not g["valid"][64:].any()
         assert np.abs(g["px"][32:64]).max() == 0.0 and np.abs(g["py"][32:64]).max() == 0.0

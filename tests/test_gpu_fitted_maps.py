@@ -122,5 +122,5 @@ def test_fitted_map_kernel_parity(gpu_lib, path):
     rays = R.gen_rays(C.CONFIGS[cfg_name]["law"], EVAL_SEED + 1, 0, (1 << 17) + 3)
     g = gpu_map(plt, m, rays)
     o = oracle.map_eval(blob, rays, threads=oracle.host_threads())
-    compare_map(g, o)
+    compare_map(g, o, blob)
     print(rel, "max logit err", float(np.abs(g["raw"][:, 0] - o["raw"][:, 0]).max()))

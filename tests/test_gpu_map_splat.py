@@ -1,6 +1,8 @@
 """GPU parity of plt_eval_map (tcgen05 fused gated MLP) and plt_splat_sensor against
 the float64 oracle.  Network tolerance: 2e-3 absolute on raw outputs at bf16
 (SURVEY A18); splat: bit-exact int64 film."""
+import math
+
 import numpy as np
 import pytest
 
@@ -35,7 +37,66 @@ def gpu_map(plt, m, rays_np, offset=0):
     return out
 
 
-def compare_map(g, o):
+def exit_ray_tolerances(o, norm, eps=TOL_NET):
+    """Per-ray bounds on the de-canonicalised outputs (a5: Eq. 10 rotation back P:321-324,
+    predict post-condition S:401) implied by a raw-output error |dy_d| <= eps (A18):
+    q_d = mid_d + half_d y_d moves by <= half_d eps; the rotation back by +phi and the
+    y-reflection are isometries, so |dp_x|, |dp_y| <= eps hypot(half_0, half_1); the
+    direction is u / |u| with u = q_{2..4}, and |a/|a| - b/|b|| <= 2 |a - b| / |a|, so
+    |dw_i| <= 2 eps |half_{2..4}| / |u|; the clamp of I to [0, 1] is 1-Lipschitz, so
+    |dI| <= eps half_5.  Plus fp32 output rounding and the fp32 angle (c, s) = p / r of the
+    kernel: 1e-6 (1 + |value|).  |u| is taken from the oracle's own raw outputs."""
+    mid, half = norm[8:14], norm[14:20]
+    y = o["raw"][:, 1:]
+    u = np.sqrt(((mid[2:5] + half[2:5] * y[:, 2:5]) ** 2).sum(1))
+    tol = {"p": eps * math.hypot(half[0], half[1]),
+           "w": 2.0 * eps * float(np.sqrt((half[2:5] ** 2).sum())) / np.maximum(u, 1e-30),
+           "I": eps * half[5]}
+    return tol
+
+
+def compare_exit_rays(g, o, norm, both):
+    """Element-wise parity of px, py, dx, dy, dz, I (a5) against oracle O10 on rays valid in
+    both with a decided mask: (1) within the bound the 2e-3 north-star tolerance implies
+    (exit_ray_tolerances); (2) consistency: each ray's output error is explained by ITS OWN
+    raw-output error through the same Lipschitz constants -- a dropped rotation, a wrong
+    reflection sign or swapped components moves outputs by O(|p|) mm and fails both."""
+    if not both.any():
+        return {}
+    mid, half = norm[8:14], norm[14:20]
+    tol = exit_ray_tolerances(o, norm)
+    dy = np.abs(g["raw"][:, 1:] - o["raw"][:, 1:])
+    rnd = lambda k: 1e-6 * (1.0 + np.abs(o[k]))
+    stats = {}
+    for k in ("px", "py"):
+        err = np.abs(g[k] - o[k])
+        assert np.all((err <= tol["p"] + rnd(k))[both]), (k, float(err[both].max()), tol["p"])
+        own = np.hypot(half[0] * dy[:, 0], half[1] * dy[:, 1]) + 4e-7 * np.hypot(o["px"], o["py"]) + rnd(k)
+        assert np.all((err <= own)[both]), (k, float((err - own)[both].max()))
+        stats["max_d" + k] = float(err[both].max())
+    y = o["raw"][:, 1:]
+    u = np.sqrt(((mid[2:5] + half[2:5] * y[:, 2:5]) ** 2).sum(1))
+    du = np.sqrt(((half[2:5] * dy[:, 2:5]) ** 2).sum(1))
+    for k in ("dx", "dy", "dz"):
+        err = np.abs(g[k] - o[k])
+        assert np.all((err <= tol["w"] + rnd(k))[both]), (k, float(err[both].max()))
+        own = 2.0 * du / np.maximum(u, 1e-30) + 4e-7 + rnd(k)
+        assert np.all((err <= own)[both]), (k, float((err - own)[both].max()))
+        stats["max_d" + k] = float(err[both].max())
+    err = np.abs(g["I"] - o["I"])
+    assert np.all((err <= tol["I"] + 1e-6)[both]), float(err[both].max())
+    assert np.all((err <= half[5] * dy[:, 5] + 1e-6)[both]), float(err[both].max())
+    stats["max_dI"] = float(err[both].max())
+    # unit direction and clamped throughput (S:401) on every valid GPU ray
+    v = g["valid"]
+    nrm = np.sqrt(g["dx"] ** 2 + g["dy"] ** 2 + g["dz"] ** 2)[v]
+    assert np.all(np.abs(nrm - 1.0) <= 2e-6), float(np.abs(nrm - 1.0).max())
+    assert np.all((g["I"][v] >= 0.0) & (g["I"][v] <= 1.0))
+    return stats
+
+
+def compare_map(g, o, blob):
+    norm = oracle.parse_map_blob(blob)["norm"]
     logit_o = o["raw"][:, 0]
     decided = np.abs(logit_o) > TOL_NET
     assert np.array_equal(g["valid"][decided], o["valid"][decided])
@@ -45,7 +106,8 @@ def compare_map(g, o):
     if both.any():
         err = np.abs(g["raw"][both, 1:] - o["raw"][both, 1:]).max()
         assert err <= TOL_NET, err
-        assert np.max(np.abs(g["I"][both] - o["I"][both])) <= TOL_NET * 0.5 + 1e-6
+    stats = compare_exit_rays(g, o, norm, both)
+    print("compare_map", {"valid": float(g["valid"].mean()), "n_both": int(both.sum()), **stats})
     inval = ~g["valid"]
     for k in ("px", "py", "dx", "dy", "dz", "I"):
         assert np.count_nonzero(g[k][inval]) == 0
@@ -58,7 +120,7 @@ def test_eval_map_ragged(gpu_lib, n):
     blob = C.map_blob("C2", 1 << 10)
     m = plt.Map(blob)
     rays = R.gen_rays(C.CONFIGS["C2"]["law"], 31, 0, n)
-    compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays))
+    compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays), blob)
 
 
 def test_eval_map_c2_2e18_and_unaligned(gpu_lib):
@@ -68,9 +130,9 @@ def test_eval_map_c2_2e18_and_unaligned(gpu_lib):
     m = plt.Map(blob, lens=gl)
     rays = R.gen_rays(C.CONFIGS["C2"]["law"], 2, 0, 1 << 18)
     o = oracle.map_eval(blob, rays, threads=oracle.host_threads())
-    v = compare_map(gpu_map(plt, m, rays), o)
+    v = compare_map(gpu_map(plt, m, rays), o, blob)
     assert 0.05 < v < 0.95
-    compare_map(gpu_map(plt, m, rays, offset=1), o)
+    compare_map(gpu_map(plt, m, rays, offset=1), o, blob)
 
 
 def test_eval_map_full_size_sampled(gpu_lib):
@@ -85,7 +147,7 @@ def test_eval_map_full_size_sampled(gpu_lib):
     sub = {k: rays[k][idx] for k in plt.RAY_KEYS}
     sub["plane_z"] = rays["plane_z"]
     o = oracle.map_eval(blob, sub, threads=oracle.host_threads())
-    compare_map({k: v[idx] for k, v in g.items()}, o)
+    compare_map({k: v[idx] for k, v in g.items()}, o, blob)
 
 
 def test_eval_map_backward_map_c3(gpu_lib):
@@ -93,7 +155,7 @@ def test_eval_map_backward_map_c3(gpu_lib):
     blob = C.map_blob("C3", 1 << 12)
     m = plt.Map(blob, lens=plt.Lens(C.lens_text("C3"), **C.CONFIGS["C3"]["opts"]))
     rays = R.gen_rays(C.CONFIGS["C3"]["law"], 3, 0, 1 << 16)
-    compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays, threads=oracle.host_threads()))
+    compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays, threads=oracle.host_threads()), blob)
 
 
 @pytest.mark.parametrize("tag", [("C2", 0), ("C3", 0), ("C4_22", 65616), ("C4_59", 16404)],
@@ -110,7 +172,7 @@ def test_eval_map_fitted_weights(gpu_lib, tag):
     if "channels" in cfg:
         law["lam"] = (400.0, 700.0)
     rays = R.gen_rays(law, 41, 0, (1 << 17) + 77)
-    v = compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays, threads=oracle.host_threads()))
+    v = compare_map(gpu_map(plt, m, rays), oracle.map_eval(blob, rays, threads=oracle.host_threads()), blob)
     assert v > 0.005
 
 
@@ -207,7 +269,7 @@ def test_splat_edges_and_scales_bit_exact(gpu_lib, scale):
 
 def test_flare_ghost_end_to_end_fp64(gpu_lib):
     """GPU fp64 trace of one ghost -> GPU splat equals the oracle splat of the GPU hits
-    (binding) and the oracle trace->splat film up to bin flips of edge rays."""
+    (binding) and the oracle trace->splat film per pixel up to bin flips of edge rays."""
     import torch
     plt = gpu_lib
     cfg = C.CONFIGS["C4_22"]
@@ -230,5 +292,64 @@ def test_flare_ghost_end_to_end_fp64(gpu_lib):
     o = oracle.trace(ol, pid, 0, rays, threads=oracle.host_threads())
     ref_o, _ = oracle.splat(FILM, o["valid"], o["px"].astype(np.float32), o["py"].astype(np.float32),
                             o["dz"].astype(np.float32), o["I"].astype(np.float32), None, scale=1.0 / n)
-    diff = np.abs(ref_o.astype(np.float64) - ref_g.astype(np.float64)).sum()
-    assert diff <= 1e-6 * max(1.0, float(ref_o.sum()))
+    # SURVEY §8(c) film rule 2, per pixel: only bin flips of rays within the fp64 parity
+    # tolerance (4e-6 mm) of a pixel edge, edge-band rays (A23) and the 2e-7 weight tolerance
+    from gpu_helpers import assert_film_within_bound, film_pixel_bound, near_edge
+    gpu = {"valid": gv, "px": h["px"].cpu().numpy().astype(np.float64), "py": h["py"].cpu().numpy().astype(np.float64),
+           "dz": h["dz"].cpu().numpy().astype(np.float64), "I": h["throughput"].cpu().numpy().astype(np.float64)}
+    b = film_pixel_bound(FILM, 1.0 / n, o, gpu, near_edge(o["margins"]), 4e-6, 2e-7)
+    st = assert_film_within_bound(ref_g, ref_o, b, max_rel_bound=0.05)
+    assert st["diff_sum_rel"] <= 1e-3
+
+
+@pytest.mark.parametrize("tag", [("C2", 0), ("C4_59", 16404), ("C4_22", 65616)], ids=lambda t: f"{t[0]}_{t[1]}")
+def test_fused_map_film_vs_oracle(gpu_lib, tag):
+    """a5 + a9 through the fused epilogue (plt_eval_map_splat) on trained weights:
+    (1) the fused film equals O11 applied to the kernel's own hits, bit for bit;
+    (2) against the oracle's O10 -> O11 film on the same rays, every pixel obeys SURVEY
+    §8(c) film rule 2 with the per-ray tolerances the 2e-3 network bound implies
+    (exit_ray_tolerances; undecided logits are ambiguous), and -- tighter -- the kernel's
+    error budget 2.5e-4 (measured <= 1.3e-4 on every fitted map), for which
+    the bound must stay below 30 % of the film's energy (a meaningful check)."""
+    import torch
+    from gpu_helpers import assert_film_within_bound, film_pixel_bound
+    plt = gpu_lib
+    name, ptag = tag
+    cfg = C.CONFIGS[name]
+    blob = C.fitted_map_blob(name, ptag)
+    norm = oracle.parse_map_blob(blob)["norm"]
+    m = plt.Map(blob, lens=plt.Lens(C.lens_text(name), **cfg["opts"]))
+    n = (1 << 17) + 91
+    if "channels" in cfg:
+        rays = C.flare_rays(name, 1, 0, n)
+        fd = {"width_px": 96, "height_px": 64, "channels": 1, "sensor_w_mm": 24.0, "sensor_h_mm": 16.0,
+              "center_x_mm": 0.0, "center_y_mm": 0.0}
+    else:
+        rays = R.gen_rays(cfg["law"], 43, 0, n)
+        fd = {"width_px": 72, "height_px": 72, "channels": 1, "sensor_w_mm": 36.0, "sensor_h_mm": 36.0,
+              "center_x_mm": 0.0, "center_y_mm": 0.0}
+    scale = 1.0 / n
+    d = plt.rays_to_device(rays)
+    h = plt.alloc_hits(n)
+    raw = torch.empty(7 * n, dtype=torch.float32, device="cuda")
+    film = torch.zeros(fd["height_px"] * fd["width_px"], dtype=torch.int64, device="cuda")
+    plt.eval_map(m, d, h, raw=raw, splat={"film_desc": fd, "film": film, "weight_scale": scale})
+    torch.cuda.synchronize()
+    g = {k: h[k].cpu().numpy().astype(np.float64) for k in ("px", "py", "dx", "dy", "dz", "throughput")}
+    g["I"] = g.pop("throughput")
+    g["valid"] = unpack_mask(h["mask_bits"].cpu().numpy(), n)
+    g["raw"] = raw.cpu().numpy().reshape(7, n).T.astype(np.float64)
+    f_gpu = film.cpu().numpy()
+    own, _ = oracle.splat(fd, g["valid"], h["px"].cpu().numpy(), h["py"].cpu().numpy(), h["dz"].cpu().numpy(),
+                          h["throughput"].cpu().numpy(), None, scale=scale)
+    assert np.array_equal(f_gpu, own.reshape(-1)), "fused film != O11 of the kernel's hits"
+    o = oracle.map_eval(blob, rays, threads=oracle.host_threads())
+    compare_map(g, o, blob)
+    f_ora, _ = oracle.splat(fd, o["valid"], o["px"].astype(np.float32), o["py"].astype(np.float32),
+                            o["dz"].astype(np.float32), o["I"].astype(np.float32), None, scale=scale)
+    ambiguous = np.abs(o["raw"][:, 0]) <= TOL_NET
+    for eps, rel in ((TOL_NET, None), (2.5e-4, 0.3)):
+        tol = exit_ray_tolerances(o, norm, eps)
+        tol_wt = np.maximum(tol["w"], tol["I"]) + 1e-6
+        b = film_pixel_bound(fd, scale, o, g, ambiguous, tol["p"] + 1e-6 * (1 + np.hypot(o["px"], o["py"])), tol_wt)
+        assert_film_within_bound(f_gpu, f_ora, b, max_rel_bound=rel)

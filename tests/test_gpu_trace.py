@@ -153,3 +153,57 @@ def test_invalid_path_id_and_empty(gpu_lib):
     with pytest.raises(plt.PltError):
         plt.trace_rays(gl, 1 << 9, d, h)              # too few interactions
     plt.trace_rays(gl, 1 << 10, d, h, n=0)            # n == 0 is a no-op
+
+
+@pytest.mark.parametrize("housing", [11.0, 9.0])
+def test_housing_cylinder_parity(gpu_lib, housing):
+    """Housing absorption (A5) on the GPU: the C2 lens inside a barrel of
+    radius 11 / 9 mm (smaller than the 12.6 / 11.5 / 10 mm clear apertures it crosses), fp32
+    all-T (JIT), fp64 all-T and an fp64 ghost against the oracle's housing branch (pinned in
+    tests/test_oracle_branches.py).  The barrel must actually decide rays: a share of
+    the rays valid without it become invalid with it."""
+    plt = gpu_lib
+    cfg = C.CONFIGS["C2"]
+    opts = dict(cfg["opts"], housing_radius_mm=housing)
+    gl, ol = _lenses(plt, "dgauss50", opts)
+    _, ol0 = _lenses(plt, "dgauss50", cfg["opts"])
+    rays = R.gen_rays(cfg["law"], 77, 0, (1 << 18) + 5)
+    o = oracle.trace(ol, 1 << 10, 0, rays, threads=oracle.host_threads())
+    o0 = oracle.trace(ol0, 1 << 10, 0, rays, threads=oracle.host_threads())
+    absorbed = o0["valid"] & ~o["valid"]
+    assert absorbed.mean() > 0.01, absorbed.mean()
+    assert not (o["valid"] & ~o0["valid"]).any()
+    compare_trace(gpu_trace(plt, gl, 1 << 10, rays, precision=0), o)
+    compare_trace(gpu_trace(plt, gl, 1 << 10, rays, precision=1), o, tol_p=4e-6, tol_w=2e-7, tol_i=2e-7)
+    pid = oracle.ghost_id(10, 7, 3)
+    og = oracle.trace(ol, pid, 0, rays, threads=oracle.host_threads())
+    st = compare_trace(gpu_trace(plt, gl, pid, rays, precision=1), og, tol_p=4e-6, tol_w=2e-7, tol_i=2e-7)
+    assert st["n_both"] > 100
+    s32 = compare_trace(gpu_trace(plt, gl, pid, rays, precision=0), og, assert_ok=False)
+    assert s32["mask_mismatch"] <= max(2, int(1e-3 * og["valid"].sum()))
+
+
+def test_housing_and_rectangle_scalar_kernel_subprocess():
+    """The scalar (non-packed, non-JIT) fp32 kernel through the same housing + CMOS-rectangle
+    cases: PLT_TRACE_X1 / PLT_TRACE_JIT=0 are read once per process, so run a child."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle, paper_2605_04017_b200 as plt
+from plt_inputs import configs as C, rays as R
+from gpu_helpers import compare_trace, gpu_trace
+cfg = C.CONFIGS["C4_22"]
+for opts in (dict(cfg["opts"], housing_radius_mm=10.0), cfg["opts"]):
+    gl = plt.Lens(C.lens_text("C4_22"), **opts); ol = oracle.load_lens(C.lens_text("C4_22"), opts)
+    rays = C.flare_rays("C4_22", 1, 0, 1 << 16)
+    o = oracle.trace(ol, 1 << 12, 0, rays)
+    compare_trace(gpu_trace(plt, gl, 1 << 12, rays, precision=0), o)
+print("ok")
+'''
+    env = dict(os.environ, PLT_TRACE_X1="1", PLT_TRACE_JIT="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
