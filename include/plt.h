@@ -185,8 +185,11 @@ typedef struct {
  * (directional operator d_{L,sigma}), unpolarised Fresnel R/T with Sellmeier/Abbe/
  * Cauchy dispersion (f_{L,sigma}); valid iff sigma_{K+1} is the output plane
  * and, for PLT_FORWARD with a sensor rectangle, the hit lies inside it.
- * Errors: PLT_E_INVALID_ARG (null pointers, n < 0, path id inconsistent with the
- * lens, > 48 steps), PLT_E_CUDA.  n == 0 is a no-op.
+ * Errors: PLT_E_INVALID_ARG (null pointers, n < 0, n >= 2^31, path id inconsistent
+ * with the lens, a path program of more than 72 surface steps), PLT_E_CUDA.  n == 0 is
+ * a no-op.  Which kernel runs a PLT_FP32 trace (run-time specialised, generic packed,
+ * scalar) is reported by plt_trace_kernel; their outputs agree with the oracle within the
+ * same tolerances but not bit for bit.
  */
 PLT_API plt_status plt_trace_rays(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
                           const plt_rays* in, const plt_hits* out, int64_t n, void* cuda_stream);
@@ -195,10 +198,12 @@ PLT_API plt_status plt_trace_rays(const plt_lens* lens, uint64_t path_id, plt_di
  * Load one path's factorised map: a binary valid-mask classifier
  * g: 4 -> 32 -> 32 -> 1 and a regressor f: 4 -> 32^5 -> 6, tanh hidden layers,
  * linear outputs.  Blob layout (little-endian): magic
- * "PLTMAP01", u32 version=1, u32 direction, u64 path_id, u32 n_cls_layers=3,
- * u32 n_reg_layers=6, f32 in_lo[4], in_hi[4], out_mid[6], out_half[6], then per
- * layer u32 out, u32 in, bf16 W[out][in], f32 b[out].  `lens` may be NULL (no
- * cross-check); otherwise the blob's path id must be consistent with the lens.
+ * "PLTMAP01", u32 version (1 or 2), u32 direction, u64 path_id, u32 n_cls_layers=3,
+ * u32 n_reg_layers=6, [version 2: f64 plane_z_mm, the input plane the map was trained
+ * on], f32 in_lo[4], in_hi[4], out_mid[6], out_half[6], then per layer u32 out, u32 in,
+ * bf16 W[out][in], f32 b[out].  `lens` may be NULL (no cross-check); otherwise the
+ * blob's path id must be consistent with the lens.  plt_eval_map rejects rays whose
+ * plane_z_mm differs from a version-2 map's plane (PLT_E_INVALID_ARG).
  * Errors: PLT_E_PARSE (truncated / bad magic), PLT_E_VALIDATION (dimensions), PLT_E_OOM.
  */
 PLT_API plt_status plt_map_load(const plt_lens* lens, const void* blob, size_t len, plt_map** out);
@@ -215,7 +220,8 @@ PLT_API void plt_map_free(plt_map* map);
  * raw_out (nullable, device, 7*n floats, SoA: raw_out[k*n + i] with k = 0 the
  * classifier logit and k = 1..6 the regressor outputs y before de-normalisation,
  * y = 0 for invalid rays) exposes the network outputs for parity.
- * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ * Errors: PLT_E_INVALID_ARG (also: in->plane_z_mm is not the plane a version-2 map was
+ * trained on), PLT_E_CUDA.
  */
 PLT_API plt_status plt_eval_map(const plt_map* map, const plt_rays* in, const plt_hits* out,
                         float* raw_out, int64_t n, void* cuda_stream);
@@ -275,6 +281,27 @@ PLT_API plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, co
  */
 PLT_API plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir dir, void* buf,
                                        size_t capacity, size_t* size);
+
+/*
+ * Which kernel plt_trace_rays launches for (lens, path_id, dir, prec) in this process:
+ * PLT_KERNEL_JIT -- the float32 kernel specialised at run time for the path program
+ * (NVRTC, all-transmission paths; compiled and cached by this call if needed);
+ * PLT_KERNEL_PACKED -- the generic packed float32 kernel (ghost paths, or all-T paths when
+ * NVRTC is unavailable); PLT_KERNEL_SCALAR -- the one-ray-per-thread float32 kernel
+ * (developer switch PLT_TRACE_X1); PLT_KERNEL_FP64 -- PLT_FP64 traces.  All are within the
+ * parity tolerances of the oracle, but their float32 results differ in the last bits, so a
+ * caller that needs reproducibility across hosts checks this.
+ * Errors: PLT_E_INVALID_ARG (null, bad enum, path id inconsistent with the lens), PLT_E_CUDA.
+ */
+typedef enum {
+    PLT_KERNEL_JIT = 0,
+    PLT_KERNEL_PACKED = 1,
+    PLT_KERNEL_SCALAR = 2,
+    PLT_KERNEL_FP64 = 3
+} plt_kernel_kind;
+
+PLT_API plt_status plt_trace_kernel(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                                    plt_kernel_kind* kind);
 
 /*
  * Backward camera integrand with a procedural scene (Eq. 9,
@@ -338,12 +365,15 @@ PLT_API plt_status plt_shade_cards(const plt_scene_card* cards, int n_cards, dou
  * precomputed map): o' = o + ((z_t - z_in)/w_z) w in float32 (round-to-nearest,
  * one fma per coordinate), w and lambda copied.  in->plane_z_mm is z_in; out's arrays
  * (device, n each, may alias in's) receive the rays; out->plane_z_mm is not used.
- * in->dz NULL: w_z = +-sqrt(max(0, 1 - w_x^2 - w_y^2)) pointing towards z_t; out->dz
- * may then be NULL too (the output stays in the (dx, dy) parameterisation).
- * Errors: PLT_E_INVALID_ARG, PLT_E_CUDA.
+ * The ray moves along its own line, forwards or backwards (t may be negative: a sensor
+ * shifted past the map's input plane).  in->dz NULL: w_z = sign * sqrt(max(0, 1 - w_x^2 -
+ * w_y^2)) with the sign of the query direction `dir` (+ for PLT_FORWARD, - for
+ * PLT_BACKWARD) -- the same rule as plt_trace_rays -- and out->dz may then be NULL
+ * too (the output stays in the (dx, dy) parameterisation).
+ * Errors: PLT_E_INVALID_ARG (also a bad dir), PLT_E_CUDA.
  */
-PLT_API plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, int64_t n,
-                                      void* cuda_stream);
+PLT_API plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, plt_dir dir,
+                                      int64_t n, void* cuda_stream);
 
 /* out[i] = film[i] * 2^-32 * scale (float), for channels*height*width pixels. */
 PLT_API plt_status plt_film_resolve(const plt_film_desc* film_desc, const int64_t* film, float* out,

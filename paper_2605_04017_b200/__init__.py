@@ -30,7 +30,7 @@ EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
             "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_shade_cards",
-            "plt_propagate_rays", "plt_lens_pupils")
+            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel")
 
 
 class PltError(RuntimeError):
@@ -103,12 +103,13 @@ def load():
     L.plt_shade_plane.argtypes = [p, d, p, i, i64, C.c_float, p, i64, p]
     L.plt_shade_plane_weighted.argtypes = [p, d, p, i, i64, C.c_float, p, p, i64, p]
     L.plt_shade_cards.argtypes = [p, i, d, d, p, i, i64, C.c_float, p, p, i64, p]
-    L.plt_propagate_rays.argtypes = [p, p, d, i64, p]
+    L.plt_propagate_rays.argtypes = [p, p, d, i, i64, p]
+    L.plt_trace_kernel.argtypes = [p, u64, i, i, p]
     L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
               "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted",
-              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils"):
+              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -379,13 +380,27 @@ def shade_cards(cards: list, background: float, z_hits_mm: float, hits: dict, fi
                                   _ptr(film, pixels, torch.int64), n, _stream(stream)))
 
 
-def propagate_rays(rays: dict, out: dict, z_target_mm: float, n: int | None = None, stream=None):
-    """plt_propagate_rays: free-space propagation to z = z_target_mm (out may alias rays)."""
+def propagate_rays(rays: dict, out: dict, z_target_mm: float, direction: int = FORWARD, n: int | None = None,
+                   stream=None):
+    """plt_propagate_rays: free-space propagation to z = z_target_mm along each ray's line
+    (out may alias rays); `direction` gives the sign of w_z for rays without dz."""
     n = _n_of(rays, n)
     r = _rays_struct(rays, n)
     o = _rays_struct(dict(out, plane_z=z_target_mm), n)
-    _check(load().plt_propagate_rays(C.byref(r), C.byref(o), float(z_target_mm), n, _stream(stream)))
+    _check(load().plt_propagate_rays(C.byref(r), C.byref(o), float(z_target_mm), int(direction), n,
+                                     _stream(stream)))
     out["plane_z"] = float(z_target_mm)
+
+
+KERNEL_KINDS = {0: "jit", 1: "packed", 2: "scalar", 3: "fp64"}
+
+
+def trace_kernel(lens: "Lens", path_id: int, direction: int = FORWARD, precision: int = FP32) -> str:
+    """plt_trace_kernel: which kernel plt_trace_rays runs for this path in this process
+    ("jit", "packed", "scalar" or "fp64")."""
+    k = C.c_int(-1)
+    _check(load().plt_trace_kernel(lens.handle, int(path_id), int(direction), int(precision), C.byref(k)))
+    return KERNEL_KINDS[k.value]
 
 
 def film_resolve(film_d: dict, film, out, scale: float = 1.0, stream=None):

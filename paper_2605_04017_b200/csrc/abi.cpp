@@ -9,12 +9,23 @@
 #include <string>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "host.h"
 
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around every compute entry point (header-only NVTX3: a no-op unless a
+// profiler injects itself), so ncu / nsys timelines name the ABI call of each kernel.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PLT_RANGE(name) NvtxRange plt_nvtx_range_(name)
 
 plt_status set_err(plt_status c, const std::string& m) {
     g_err = m;
@@ -157,6 +168,7 @@ plt_status plt_trace_rays_splat(const plt_lens* lens, uint64_t path_id, plt_dir 
 static plt_status trace_impl(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
                              const plt_rays* in, const plt_hits* out, const plt_splat_target* splat, int64_t n,
                              void* cuda_stream) {
+    PLT_RANGE(splat ? "plt_trace_rays_splat" : "plt_trace_rays");
     PLT_GUARD_BEGIN
     if (!lens) return set_err(PLT_E_INVALID_ARG, "lens is null");
     if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
@@ -203,12 +215,17 @@ plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, const plt_
 
 static plt_status eval_map_impl(const plt_map* map, const plt_rays* in, const plt_hits* out, float* raw_out,
                                 const plt_splat_target* splat, int64_t n, void* cuda_stream) {
+    PLT_RANGE(splat ? "plt_eval_map_splat" : "plt_eval_map");
     PLT_GUARD_BEGIN
     if (!map) return set_err(PLT_E_INVALID_ARG, "map is null");
     if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
     if (n == 0) return PLT_OK;
     if (!rays_ok(in) || !hits_ok(out)) return set_err(PLT_E_INVALID_ARG, "null ray/hit pointer");
     if (n >= (int64_t)1 << 31) return set_err(PLT_E_INVALID_ARG, "n must be < 2^31 per call");
+    if (map->has_plane && std::fabs(in->plane_z_mm - map->plane_z) > 1e-6 * (1.0 + std::fabs(map->plane_z)))
+        return set_err(PLT_E_INVALID_ARG, "rays lie on the plane z = " + std::to_string(in->plane_z_mm) +
+                                              " mm but the map was trained on z = " + std::to_string(map->plane_z) +
+                                              " mm (move them with plt_propagate_rays)");
     plt::SplatCtx sc;
     plt_status s = splat_target(splat, &sc);
     if (s != PLT_OK) return s;
@@ -237,6 +254,7 @@ static plt_status eval_map_impl(const plt_map* map, const plt_rays* in, const pl
 
 plt_status plt_splat_sensor(const plt_film_desc* fd, int64_t* film, const plt_hits* hits, const uint8_t* channel,
                             float weight_scale, int64_t n, unsigned long long* dropped, void* cuda_stream) {
+    PLT_RANGE("plt_splat_sensor");
     PLT_GUARD_BEGIN
     if (!fd || !film || !hits) return set_err(PLT_E_INVALID_ARG, "null film/hits");
     if (!film_desc_ok(fd)) return set_err(PLT_E_INVALID_ARG, "bad film description");
@@ -268,9 +286,25 @@ plt_status plt_trace_jit_cubin(const plt_lens* lens, uint64_t path_id, plt_dir d
     PLT_GUARD_END
 }
 
+plt_status plt_trace_kernel(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                            plt_kernel_kind* kind) {
+    PLT_GUARD_BEGIN
+    if (!lens || !kind) return set_err(PLT_E_INVALID_ARG, "lens and kind must be non-null");
+    if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
+    if (prec != PLT_FP32 && prec != PLT_FP64) return set_err(PLT_E_INVALID_ARG, "bad precision");
+    auto cp = plt::compile_path(*lens, path_id, (int)dir);
+    if (prec == PLT_FP64) { *kind = PLT_KERNEL_FP64; return PLT_OK; }
+    plt_status s = check_device();   // the JIT compiles for, and loads on, the current device
+    if (s != PLT_OK) return s;
+    *kind = (plt_kernel_kind)plt::trace_fp32_kind(cp->pf, nullptr);
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
 static plt_status shade_impl(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits, int spp,
                              int64_t pixels, float weight_scale, const float* in_dz, int64_t* film, int64_t n,
                              void* cuda_stream) {
+    PLT_RANGE("plt_shade_plane");
     PLT_GUARD_BEGIN
     if (!scene || !hits || !film) return set_err(PLT_E_INVALID_ARG, "null scene/hits/film");
     if (!(scene->period_mm > 0) || !std::isfinite(scene->z_mm) || !std::isfinite(scene->contrast) ||
@@ -297,6 +331,7 @@ plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_mm, const
 plt_status plt_shade_cards(const plt_scene_card* cards, int n_cards, double background, double z_hits_mm,
                            const plt_hits* hits, int spp, int64_t pixels, float weight_scale, const float* in_dz,
                            int64_t* film, int64_t n, void* cuda_stream) {
+    PLT_RANGE("plt_shade_cards");
     PLT_GUARD_BEGIN
     if (!cards || !hits || !film) return set_err(PLT_E_INVALID_ARG, "null cards/hits/film");
     if (n_cards < 1 || n_cards > plt::kMaxCards) return set_err(PLT_E_INVALID_ARG, "n_cards must be 1..8");
@@ -331,9 +366,11 @@ plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double z_hits_
     return shade_impl(scene, z_hits_mm, hits, spp, pixels, weight_scale, in_dz, film, n, cuda_stream);
 }
 
-plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, int64_t n,
+plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, plt_dir dir, int64_t n,
                               void* cuda_stream) {
+    PLT_RANGE("plt_propagate_rays");
     PLT_GUARD_BEGIN
+    if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
     if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
     if (n == 0) return PLT_OK;
     if (!rays_ok(in) || !out || !out->ox || !out->oy || !out->dx || !out->dy || (in->dz && !out->dz) || !out->lambda_nm ||
@@ -341,11 +378,14 @@ plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_
         return set_err(PLT_E_INVALID_ARG, "null ray pointer or non-finite plane");
     plt_status s = check_device();
     if (s != PLT_OK) return s;
-    return cuda_status(plt::launch_propagate(*in, *out, (float)z_target_mm, n, cuda_stream), "propagate_rays");
+    return cuda_status(plt::launch_propagate(*in, *out, (float)z_target_mm, dir == PLT_BACKWARD ? -1.f : 1.f, n,
+                                             cuda_stream),
+                       "propagate_rays");
     PLT_GUARD_END
 }
 
 plt_status plt_film_resolve(const plt_film_desc* fd, const int64_t* film, float* out, double scale, void* cuda_stream) {
+    PLT_RANGE("plt_film_resolve");
     PLT_GUARD_BEGIN
     if (!fd || !film || !out) return set_err(PLT_E_INVALID_ARG, "null film/out");
     if (fd->width_px <= 0 || fd->height_px <= 0 || fd->channels <= 0) return set_err(PLT_E_INVALID_ARG, "bad film description");

@@ -106,16 +106,17 @@ __global__ void __launch_bounds__(kThreads) shade_cards_kernel(const __grid_cons
     }
 }
 
-__global__ void __launch_bounds__(kThreads) propagate_kernel(plt_rays in, plt_rays out, float z_target, int64_t n) {
+__global__ void __launch_bounds__(kThreads) propagate_kernel(plt_rays in, plt_rays out, float z_target, float sdir,
+                                                              int64_t n) {
     const float z0 = (float)in.plane_z_mm;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
         const float dx = in.dx[i], dy = in.dy[i];
         float dz;
         if (in.dz) {
             dz = in.dz[i];
-        } else {   // omega in S^2_+  given by (dx, dy), pointing towards the target plane
+        } else {   // omega in S^2_+  given by (dx, dy), with the sign of the query direction
             const float m = sqrtf(fmaxf(0.f, fmaf(-dx, dx, fmaf(-dy, dy, 1.f))));
-            dz = z_target < z0 ? -m : m;
+            dz = sdir * m;
         }
         const float t = __fdiv_rn(__fsub_rn(z_target, z0), dz);
         const float lam = in.lambda_nm[i], ox = __fmaf_rn(t, dx, in.ox[i]), oy = __fmaf_rn(t, dy, in.oy[i]);
@@ -154,8 +155,8 @@ int launch_shade_cards(const SceneCards& sc, double z_hits, const plt_hits& hits
     return (int)cudaGetLastError();
 }
 
-int launch_propagate(const plt_rays& in, const plt_rays& out, float z_target, int64_t n, void* stream) {
-    propagate_kernel<<<blocks_for(n), kThreads, 0, (cudaStream_t)stream>>>(in, out, z_target, n);
+int launch_propagate(const plt_rays& in, const plt_rays& out, float z_target, float sdir, int64_t n, void* stream) {
+    propagate_kernel<<<blocks_for(n), kThreads, 0, (cudaStream_t)stream>>>(in, out, z_target, sdir, n);
     return (int)cudaGetLastError();
 }
 

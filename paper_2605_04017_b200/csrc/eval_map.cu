@@ -40,6 +40,7 @@ namespace plt {
 namespace {
 
 constexpr int kTile = 128;                   // rays per tile (UMMA M)
+constexpr int kGroups = 8;                   // tile pipelines per SM (8 x 64 TMEM columns = 512)
 constexpr int kQueue = 256;                  // per-group queue capacity (ring of ray indices)
 constexpr int kACols = 32;                   // A operand in TMEM: 64 bf16 per row = 32 columns
                                              // (cols 0-15 hi, 16-31 lo); the bias K-step reads a
@@ -161,53 +162,8 @@ __device__ __forceinline__ float tanh_accurate(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
     return fmaf(-2.f, r, 1.f);
 }
-// Odd/even rational tanh(x) = x P(x^2) / Q(x^2) on [-9, 9] (|error| <~ 4e-7 in fp32; the
-// paper's own inference also uses a rational tanh): one MUFU rcp per value, the
-// polynomials in packed FFMA2 (two activations per instruction).
-__device__ __forceinline__ float2 tanh_rational2(float2 x) {
-    x.x = fminf(fmaxf(x.x, -9.f), 9.f);
-    x.y = fminf(fmaxf(x.y, -9.f), 9.f);
-    const float2 x2 = __fmul2_rn(x, x);
-    auto c = [](float v) { return make_float2(v, v); };
-    float2 p = __ffma2_rn(x2, c(-2.76076847742355e-16f), c(2.00018790482477e-13f));
-    p = __ffma2_rn(x2, p, c(-8.60467152213735e-11f));
-    p = __ffma2_rn(x2, p, c(5.12229709037114e-08f));
-    p = __ffma2_rn(x2, p, c(1.48572235717979e-05f));
-    p = __ffma2_rn(x2, p, c(6.37261928875436e-04f));
-    p = __ffma2_rn(x2, p, c(4.89352455891786e-03f));
-    p = __fmul2_rn(p, x);
-    float2 q = __ffma2_rn(x2, c(1.19825839466702e-06f), c(1.18534705686654e-04f));
-    q = __ffma2_rn(x2, q, c(2.26843463243900e-03f));
-    q = __ffma2_rn(x2, q, c(4.89352518554385e-03f));
-    float2 r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(q.x));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(q.y));
-    return __fmul2_rn(p, r);
-}
-// tanh via one MUFU ex2 and a reciprocal by Newton iterations on the FMA pipe (packed):
-// d = 1 + e in [1, 2^26] (x clamped to 9), r0 from the exponent bit trick (~1/8 relative),
-// three Newton steps (error 2^-3 -> 2^-6 -> 2^-12 -> 2^-24).
-__device__ __forceinline__ float2 tanh_ex2_newton2(float2 x) {
-    x.x = fminf(x.x, 9.f);
-    x.y = fminf(x.y, 9.f);
-    const float2 a = __fmul2_rn(x, make_float2(2.8853900817779268f, 2.8853900817779268f));
-    float2 e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a.x));
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a.y));
-    const float2 one = make_float2(1.f, 1.f), two = make_float2(2.f, 2.f);
-    const float2 d = __fadd2_rn(e, one);
-    float2 r = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(d.x)),
-                           __int_as_float(0x7EF311C3 - __float_as_int(d.y)));
-    const float2 nd = make_float2(-d.x, -d.y);
-#pragma unroll
-    for (int it = 0; it < 3; ++it) r = __fmul2_rn(r, __ffma2_rn(nd, r, two));
-    return __ffma2_rn(make_float2(-2.f, -2.f), r, one);
-}
 #ifndef PLT_MAP_CLS_ACCURATE_UNITS
 #define PLT_MAP_CLS_ACCURATE_UNITS 16   // most logit-influential classifier h1 units with the accurate tanh
-#endif
-#ifndef PLT_MAP_CLS_TANH
-#define PLT_MAP_CLS_TANH 1   // classifier first hidden layer: 0 MUFU tanh, 1 ex2+rcp, 2 rational
 #endif
 // pack (lo_elem, hi_elem) -> bf16x2 with lo_elem in the low half (lower address)
 __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
@@ -499,22 +455,10 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             PLT_CLK(h1);
             // the classifier's h1 units are ordered by influence on the logit (map.cpp):
             // the first PLT_MAP_CLS_ACCURATE_UNITS take the accurate tanh
-            if (accurate && PLT_MAP_CLS_TANH == 1 && 16 * half < PLT_MAP_CLS_ACCURATE_UNITS) {
+            if (accurate && 16 * half < PLT_MAP_CLS_ACCURATE_UNITS) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
                     v[j] = 16 * half + j < PLT_MAP_CLS_ACCURATE_UNITS ? tanh_accurate(v[j]) : tanh_approx(v[j]);
-            } else if (accurate && PLT_MAP_CLS_TANH == 3) {
-#pragma unroll
-                for (int j = 0; j < 16; j += 2) {
-                    const float2 y = tanh_ex2_newton2(make_float2(v[j], v[j + 1]));
-                    v[j] = y.x; v[j + 1] = y.y;
-                }
-            } else if (accurate && PLT_MAP_CLS_TANH == 2) {
-#pragma unroll
-                for (int j = 0; j < 16; j += 2) {
-                    const float2 y = tanh_rational2(make_float2(v[j], v[j + 1]));
-                    v[j] = y.x; v[j + 1] = y.y;
-                }
             } else {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
@@ -726,7 +670,6 @@ int launch_groups(const Params& P, int sms, cudaStream_t stream) {
 
 int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams& mp, const plt_rays& in,
                     const plt_hits& out, float* raw, int64_t n, void* stream, const SplatCtx& sc) {
-    static thread_local int warm_dev = -1;   // keep the stream-ordered pool's memory (no cudaMalloc per call)
     if (lay.total_bytes > kMaxImageBytes) return (int)cudaErrorInvalidValue;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -743,33 +686,17 @@ int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams
     P.mp = mp;
     P.wimg = (const uint8_t*)d_weights;
     P.sc = sc;
-    static const int groups = [] {
-        const char* e = getenv("PLT_MAP_GROUPS");   // tuning knob (4, 6, 7 or 8 tile pipelines per SM)
-        return e ? atoi(e) : 8;
-    }();
-    cudaStream_t s = (cudaStream_t)stream;
-    if (warm_dev != dev) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        warm_dev = dev;
-    }
-    // tile counter from the stream-ordered pool (no host synchronisation; capture-safe)
-    void* ctr = nullptr;
-    cudaError_t e = cudaMallocAsync(&ctr, 256, s);
+    // tile counter from the library's stream-ordered pool (no host synchronisation;
+    // capture-safe; freed on every exit path)
+    ScratchGuard scratch(stream);
+    cudaError_t e = (cudaError_t)scratch.alloc(256);
     if (e != cudaSuccess) return (int)e;
-    e = cudaMemsetAsync(ctr, 0, 256, s);
+    e = cudaMemsetAsync(scratch.p, 0, 256, (cudaStream_t)stream);
     if (e != cudaSuccess) return (int)e;
-    P.tile_ctr = (int*)ctr;
-    int rc;
-    if (groups == 4) rc = launch_groups<4>(P, sms, s);
-    else if (groups == 6) rc = launch_groups<6>(P, sms, s);
-    else if (groups == 7) rc = launch_groups<7>(P, sms, s);
-    else rc = launch_groups<8>(P, sms, s);
-    const cudaError_t fe = cudaFreeAsync(ctr, s);
-    return rc != 0 ? rc : (int)fe;
+    P.tile_ctr = (int*)scratch.p;
+    const int rc = launch_groups<kGroups>(P, sms, (cudaStream_t)stream);
+    const int fe = scratch.release();
+    return rc != 0 ? rc : fe;
 }
 
 }  // namespace plt

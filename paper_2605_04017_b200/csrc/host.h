@@ -61,6 +61,8 @@ struct plt_lens {
 struct plt_map {
     uint32_t direction = 0;
     uint64_t path_id = 0;
+    bool has_plane = false;   // blob version >= 2: the input plane the map was trained on
+    double plane_z = 0;       // (eval_map rejects rays on any other plane)
     plt::MapLayout layout{};
     plt::MapParams params{};
     std::vector<uint8_t> image;            // packed host weight image (layout.total_bytes)

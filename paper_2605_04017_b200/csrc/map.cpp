@@ -91,10 +91,15 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
     r.off = 8;
     auto m = std::make_unique<plt_map>();
     const uint32_t ver = r.get<uint32_t>("version");
-    if (ver != 1) fail(PLT_E_PARSE, "unsupported map version " + std::to_string(ver));
+    if (ver != 1 && ver != 2) fail(PLT_E_PARSE, "unsupported map version " + std::to_string(ver));
     m->direction = r.get<uint32_t>("direction");
     m->path_id = r.get<uint64_t>("path_id");
     const uint32_t ncl = r.get<uint32_t>("n_cls_layers"), nrl = r.get<uint32_t>("n_reg_layers");
+    if (ver >= 2) {   // version 2 records the input plane the map was trained on (rays' plane_z)
+        m->plane_z = r.get<double>("plane_z_mm");
+        if (!std::isfinite(m->plane_z)) fail(PLT_E_VALIDATION, "map input plane z must be finite");
+        m->has_plane = true;
+    }
     if (ncl != 3 || nrl != 6)
         fail(PLT_E_VALIDATION, "map must have 3 classifier and 6 regressor layers (P:391-392)");
     if (m->direction > 1) fail(PLT_E_VALIDATION, "map direction must be 0 or 1");

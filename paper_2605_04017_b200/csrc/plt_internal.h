@@ -106,6 +106,7 @@ struct SplatCtx {
     int width, height, channels;
     float scale;
     float cxf, cyf, hwf, hhf, sxf, syf;   // fp32 fast-path constants
+    float guard;                          // fp32 pixel-coordinate error bound (px), see make_splat_ctx
 };
 
 inline SplatCtx make_splat_ctx(const plt_film_desc& fd, int64_t* film, const uint8_t* channel, float scale,
@@ -118,8 +119,38 @@ inline SplatCtx make_splat_ctx(const plt_film_desc& fd, int64_t* film, const uin
     c.cxf = (float)fd.center_x_mm; c.cyf = (float)fd.center_y_mm;
     c.hwf = (float)(0.5 * c.W); c.hhf = (float)(0.5 * c.H);
     c.sxf = (float)(fd.width_px / c.W); c.syf = (float)(fd.height_px / c.H);
+    // Error of the fp32 pixel coordinate (px - cxf + hwf) * sxf against the exact double
+    // expression of O11, for hits inside (or near) the film: each of cxf, hwf, sxf and the
+    // three roundings contributes <= 2^-24 relative to a term of magnitude <= |c| s + 2
+    // width (in px), i.e. <= ((|cx| + |cy|) max(sx, sy) + 5 max(width, height)) 2^-24 with
+    // headroom x2; never below the historical 2e-3 px.  Hits closer than this to a pixel
+    // edge take the double path, so the film stays bit-identical for any film size.
+    {
+        const double s = fd.width_px / c.W > fd.height_px / c.H ? fd.width_px / c.W : fd.height_px / c.H;
+        const double m = fd.width_px > fd.height_px ? fd.width_px : fd.height_px;
+        const double ac = (c.cx < 0 ? -c.cx : c.cx) + (c.cy < 0 ? -c.cy : c.cy);
+        const double g = 2.0 * (ac * s + 5.0 * m) * 5.9604644775390625e-8;
+        c.guard = (float)(g > 2e-3 ? g : 2e-3);
+    }
     return c;
 }
+
+#ifndef PLT_JIT
+// Stream-ordered scratch from the library's own per-device pool (runtime.cpp); both
+// return cudaError_t as int.  ScratchGuard frees on every exit path of a launcher.
+int scratch_alloc(void** p, size_t bytes, void* stream);
+int scratch_free(void* p, void* stream);
+struct ScratchGuard {
+    void* p = nullptr;
+    void* stream = nullptr;
+    explicit ScratchGuard(void* s) : stream(s) {}
+    ScratchGuard(const ScratchGuard&) = delete;
+    ScratchGuard& operator=(const ScratchGuard&) = delete;
+    int alloc(size_t bytes) { return scratch_alloc(&p, bytes, stream); }
+    int release() { const int e = scratch_free(p, stream); p = nullptr; return e; }
+    ~ScratchGuard() { if (p) scratch_free(p, stream); }
+};
+#endif
 
 int launch_trace_fp32(const Program<float>& pf, const Program<double>& pd, const plt_rays& in,
                       const plt_hits& out, int64_t n, void* stream, const SplatCtx& sc);
@@ -127,6 +158,8 @@ int launch_trace_fp64(const Program<double>& pd, const plt_rays& in, const plt_h
                       int64_t n, void* stream, const SplatCtx& sc);
 // Run-time specialised packed trace kernel for P (trace_jit.cpp): cudaKernel_t or nullptr.
 void* trace_jit_kernel(const Program<float>& P);
+// plt_kernel_kind of the float32 kernel that runs P (trace.cu); *jit receives the JIT kernel.
+int trace_fp32_kind(const Program<float>& P, void** jit);
 #ifndef PLT_JIT
 }  // namespace plt
 #include <string>
@@ -146,7 +179,7 @@ struct SceneCards {
 };
 int launch_shade_cards(const SceneCards& sc, double z_hits, const plt_hits& hits, int spp, int64_t pixels,
                        float scale, int64_t* film, int64_t n, void* stream, const float* in_dz);
-int launch_propagate(const plt_rays& in, const plt_rays& out, float z_target, int64_t n, void* stream);
+int launch_propagate(const plt_rays& in, const plt_rays& out, float z_target, float sdir, int64_t n, void* stream);
 int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
                  float scale, int64_t n, unsigned long long* dropped, void* stream);
 int launch_resolve(const plt_film_desc& fd, const int64_t* film, float* out, double scale, void* stream);

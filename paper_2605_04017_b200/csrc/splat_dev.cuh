@@ -22,14 +22,13 @@ namespace plt {
 // groups lanes with the 32-bit __match_any_sync.
 __device__ __forceinline__ int splat_key(const SplatCtx& c, float px, float py, float dz, float I, int ch,
                                          long long& w, bool& drop) {
-    constexpr float kGuard = 2e-3f;
-    // Pixel coordinate: fp32 estimate first.  Its error is < 1e-3 px for any film below
-    // 10^5 px, so when it lies more than kGuard from an integer its floor equals the
-    // floor of the exact double expression of O11; only hits near a pixel edge evaluate
-    // the double expression (bit-exact film).
+    // Pixel coordinate: fp32 estimate first.  Its error is below c.guard (derived from the
+    // film size in make_splat_ctx), so when it lies more than c.guard from an integer its
+    // floor equals the floor of the exact double expression of O11; only hits near a pixel
+    // edge evaluate the double expression (bit-exact film for any film size).
     const float fxs = (px - c.cxf + c.hwf) * c.sxf, fys = (c.hhf - (py - c.cyf)) * c.syf;
     double fxf = floorf(fxs), fyf = floorf(fys);
-    if (fabsf(fxs - rintf(fxs)) < kGuard || fabsf(fys - rintf(fys)) < kGuard) {
+    if (fabsf(fxs - rintf(fxs)) < c.guard || fabsf(fys - rintf(fys)) < c.guard) {
         const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn((double)px, c.cx), c.W * 0.5), c.W), (double)c.width);
         const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(c.H * 0.5, __dsub_rn((double)py, c.cy)), c.H), (double)c.height);
         fxf = floor(fx); fyf = floor(fy);

@@ -71,9 +71,11 @@ def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, 
     else:
         src = rays
         if map_plane_z is not None and float(map_plane_z) != float(rays["plane_z"]):
-            dst = scratch_rays if scratch_rays is not None else {k: torch.empty_like(rays[k]) for k in
-                                                                 ("ox", "oy", "dx", "dy", "dz", "lambda_nm")}
-            propagate_rays(rays, dst, map_plane_z, stream=stream)
+            # rays without dz (A32) keep that form: the scratch gets no dz array either
+            dst = scratch_rays if scratch_rays is not None else {
+                k: (torch.empty_like(rays[k]) if rays.get(k) is not None else None)
+                for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm")}
+            propagate_rays(rays, dst, map_plane_z, direction=BACKWARD, stream=stream)
             src = dst
         eval_map(m, src, h, stream=stream)
     in_dz = None

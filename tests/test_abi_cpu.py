@@ -187,9 +187,10 @@ def test_camera_entry_points_validate_then_fail_loudly(plt):
     assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 0, 100, 1.0, film, 10, None) == 1
     assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 4, 100, 1.0, None, 10, None) == 1
     assert lib.plt_shade_plane(C.byref(good), -5.0, C.byref(hits), 4, 100, 1.0, film, 0, None) == 0
-    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, 10, None) == 6
-    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), float("nan"), 10, None) == 1
-    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, -1, None) == 1
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, 0, 10, None) == 6
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), float("nan"), 0, 10, None) == 1
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, 0, -1, None) == 1
+    assert lib.plt_propagate_rays(C.byref(rays), C.byref(rays), 50.0, 2, 10, None) == 1   # bad direction
 
 
 ASPH_TABLE = """name asph_singlet
@@ -289,8 +290,8 @@ def test_rays_without_dz_pass_validation_then_fail_loudly(plt):
     assert lib.plt_trace_rays(L.handle, 1 << 10, 0, 0, C.byref(no_dx), C.byref(hits), 10, None) == 1
     assert lib.plt_eval_map(m.handle, C.byref(no_dz), C.byref(hits), None, 10, None) == 6
     full = plt.Rays(*fake[:6], -5.0)
-    assert lib.plt_propagate_rays(C.byref(no_dz), C.byref(no_dz), 50.0, 10, None) == 6
-    assert lib.plt_propagate_rays(C.byref(full), C.byref(no_dz), 50.0, 10, None) == 1
+    assert lib.plt_propagate_rays(C.byref(no_dz), C.byref(no_dz), 50.0, 1, 10, None) == 6
+    assert lib.plt_propagate_rays(C.byref(full), C.byref(no_dz), 50.0, 1, 10, None) == 1
 
 
 @pytest.mark.parametrize("kind", ["coated", "aspheric", "sellmeier"])

@@ -57,14 +57,14 @@ def test_propagate_matches_closed_form(gpu_lib):
     d = plt.rays_to_device(rays)
     out = {k: torch.empty_like(d[k]) for k in plt.RAY_KEYS}
     z0 = C.CONFIGS["C3"]["law"]["plane_z"]
-    plt.propagate_rays(d, out, z0)
+    plt.propagate_rays(d, out, z0, direction=plt.BACKWARD)
     torch.cuda.synchronize()
-    ref = oracle.propagate(rays, z0)
+    ref = oracle.propagate(rays, z0, direction=oracle.BACKWARD)
     for k in ("ox", "oy"):
         assert np.max(np.abs(out[k].cpu().numpy() - ref[k])) <= 2e-5
     for k in ("dx", "dy", "dz", "lambda_nm"):
         assert np.array_equal(out[k].cpu().numpy(), rays[k])
-    plt.propagate_rays(d, d, z0)                                       # in place (aliasing allowed)
+    plt.propagate_rays(d, d, z0, direction=plt.BACKWARD)               # in place (aliasing allowed)
     torch.cuda.synchronize()
     assert torch.equal(d["ox"], out["ox"]) and torch.equal(d["oy"], out["oy"])
 

@@ -74,3 +74,29 @@ def test_jit_out_of_range_wavelengths_take_the_exact_retrace(gpu_lib):
     compare_trace(g, o)
     out = (lam < 378.0) | (lam > 791.0)
     assert np.all(g["flags"][out] == 1)
+
+
+def test_trace_kernel_reports_the_kernel_that_runs(gpu_lib, tmp_path):
+    """plt_trace_kernel makes the kernel choice observable (the JIT and generic kernels
+    differ in the last bits): on this box all-T paths must run the run-time specialised
+    kernel (NVRTC present -- so the bench and the parity tests measure the kernel DESIGN.md
+    describes), ghosts the generic packed kernel, fp64 the float64 kernel; with
+    PLT_TRACE_JIT=0 the all-T path reports the generic kernel."""
+    plt = gpu_lib
+    cfg = C.CONFIGS["C2"]
+    lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
+    assert plt.trace_kernel(lens, lens.all_t_id()) == "jit"
+    assert plt.trace_kernel(lens, 1 << 10, precision=plt.FP64) == "fp64"
+    ghost = sorted(lens.enumerate_ghosts(2)[0])[-1]
+    assert plt.trace_kernel(lens, ghost) == "packed"
+    code = f"""
+import sys; sys.path.insert(0, {ROOT!r})
+import paper_2605_04017_b200 as plt
+from plt_inputs import configs as C
+cfg = C.CONFIGS["C2"]
+lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
+print(plt.trace_kernel(lens, lens.all_t_id()))
+"""
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PLT_TRACE_JIT="0"), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("packed"), r.stdout + r.stderr

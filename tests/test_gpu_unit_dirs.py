@@ -65,8 +65,9 @@ def test_eval_map_ignores_dz(gpu_lib):
 
 
 def test_propagate_without_dz(gpu_lib):
-    """plt_propagate_rays with in->dz == out->dz == NULL vs the float64 oracle (towards the
-    target plane; the sensor-shift focusing of P:425-427)."""
+    """plt_propagate_rays with in->dz == out->dz == NULL vs the float64 oracle: backward
+    (sensor) rays moved along their lines upstream and downstream (the sensor-shift
+    focusing of P:425-427; w_z takes the query direction's sign, as in the trace)."""
     import torch
     plt = gpu_lib
     cfg = C.CONFIGS["C3_DOF"] if "C3_DOF" in C.CONFIGS else C.CONFIGS["C3"]
@@ -76,10 +77,11 @@ def test_propagate_without_dz(gpu_lib):
     out = {k: torch.empty(n, dtype=torch.float32, device="cuda") for k in ("ox", "oy", "dx", "dy", "lambda_nm")}
     out["dz"] = None
     z0 = float(rays["plane_z"])
+    # backward sensor rays (w_z < 0) moved both downstream and upstream of their plane
     for zt in (z0 + 1.5, z0 - 1.0):
-        plt.propagate_rays(d, out, zt)
+        plt.propagate_rays(d, out, zt, direction=plt.BACKWARD)
         torch.cuda.synchronize()
-        o = oracle.propagate(rays, zt)
+        o = oracle.propagate(rays, zt, direction=oracle.BACKWARD)
         for k in ("ox", "oy"):
             err = np.abs(out[k].cpu().numpy().astype(np.float64) - o[k])
             assert err.max() < 2e-5 * (1.0 + np.abs(o[k]).max()), (zt, k, err.max())

@@ -33,6 +33,6 @@ for n in (1, 37, 4096 + 37):
     plt.eval_map(m, rays, h, splat=spl)
     plt.shade_plane({"z_mm": -1000.0, "period_mm": 50.0, "contrast": 0.1}, -5.0, h, film, 3)
     dst = {k: torch.empty_like(rays[k]) for k in plt.RAY_KEYS}
-    plt.propagate_rays(rays, dst, -4.0)
+    plt.propagate_rays(rays, dst, -4.0, direction=plt.BACKWARD)
 torch.cuda.synchronize()
 print("sanitize smoke done")
