@@ -153,6 +153,12 @@ def parse_map_blob(blob: bytes) -> dict:
         raise ValueError("bad map magic")
     ver, direction, path_id, ncl, nrl = struct.unpack_from("<IIQII", blob, 8)
     off = 8 + struct.calcsize("<IIQII")
+    if ver not in (1, 2):
+        raise ValueError(f"unsupported map version {ver}")
+    plane_z = None
+    if ver == 2:                       # the input plane the map was trained on
+        (plane_z,) = struct.unpack_from("<d", blob, off)
+        off += 8
     norm = np.frombuffer(blob, np.float32, 20, off).astype(np.float64)
     off += 80
     heads = []
@@ -170,7 +176,7 @@ def parse_map_blob(blob: bytes) -> dict:
                 dims.append(fi)
             dims.append(fo)
         heads.append({"dims": dims, "W": Ws, "b": Bs})
-    return {"version": ver, "direction": direction, "path_id": path_id, "norm": norm,
+    return {"version": ver, "direction": direction, "path_id": path_id, "norm": norm, "plane_z": plane_z,
             "classifier": heads[0], "regressor": heads[1]}
 
 
@@ -194,6 +200,8 @@ def mlp_forward(head: dict, x: np.ndarray) -> np.ndarray:
 def map_eval(model, rays: dict, threads: int = 1) -> dict:
     """O10 factorised query on float32 rays; returns valid, px..I and raw (n, 7)."""
     m = parse_map_blob(model) if isinstance(model, (bytes, bytearray)) else model
+    if m.get("plane_z") is not None and abs(float(rays["plane_z"]) - m["plane_z"]) > 1e-6 * (1 + abs(m["plane_z"])):
+        raise ValueError(f"rays on plane z = {rays['plane_z']} but the map was trained on z = {m['plane_z']}")
     ncl, cd, cW, cB = _head_arrays(m["classifier"])
     nrl, rd, rW, rB = _head_arrays(m["regressor"])
     norm = np.ascontiguousarray(m["norm"])
@@ -269,10 +277,11 @@ def shade_cards(cards: list, background: float, z_hits: float, valid, px, py, dx
     return f
 
 
-def propagate(rays: dict, z_target: float) -> dict:
-    """Free-space propagation to z = z_target in float64 (closed form o + ((z_t - z_0)/w_z) w)."""
-    towards = 1.0 if float(z_target) >= float(rays["plane_z"]) else -1.0
-    dz = _dz(rays, towards)                         # absent dz: omega in S^2_+ towards z_target
+def propagate(rays: dict, z_target: float, direction: int = FORWARD) -> dict:
+    """Free-space propagation to z = z_target in float64 (closed form o + ((z_t - z_0)/w_z) w),
+    along the ray's line in either sense.  Absent dz: omega in S^2_+  with the sign of
+    the query direction (+ forward, - backward), the rule of the trace (A32)."""
+    dz = _dz(rays, 1.0 if direction == FORWARD else -1.0)
     t = (float(z_target) - float(rays["plane_z"])) / dz
     out = {k: np.asarray(rays[k], np.float64).copy() for k in ("dx", "dy", "lambda_nm")}
     out["dz"] = dz.copy()

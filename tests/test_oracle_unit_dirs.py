@@ -49,14 +49,24 @@ def test_trace_without_dz_matches_unit_directions():
         assert np.sign(b["dz"][both]).min() == np.sign(a["dz"][both]).min()
 
 
-def test_propagate_without_dz_points_towards_the_target():
+def test_propagate_without_dz_follows_the_query_direction():
+    """Absent dz, w_z takes the sign of the query direction (A32, as the trace): a forward ray
+    moved to a plane behind it travels backwards along its own line (t < 0), a backward
+    (sensor) ray moved upstream or downstream stays on its line with w_z < 0."""
     rng = np.random.default_rng(2)
     th = rng.uniform(0, 0.3, 100)
     dx, dy = np.sin(th), np.zeros(100)
     rays = {"ox": np.zeros(100), "oy": np.zeros(100), "dx": dx, "dy": dy, "lambda_nm": np.full(100, 550.0),
             "plane_z": 10.0}
     fw = oracle.propagate(rays, 20.0)
-    bw = oracle.propagate(rays, 0.0)
+    fw_back = oracle.propagate(rays, 0.0)                       # forward ray, plane behind it
     np.testing.assert_allclose(fw["ox"], 10.0 * np.tan(th), rtol=1e-12)
-    np.testing.assert_allclose(bw["ox"], 10.0 * np.tan(th), rtol=1e-12)   # travelled towards -z
-    assert (fw["dz"] > 0).all() and (bw["dz"] < 0).all()
+    np.testing.assert_allclose(fw_back["ox"], -10.0 * np.tan(th), rtol=1e-12)
+    assert (fw["dz"] > 0).all() and (fw_back["dz"] > 0).all()
+    for zt, sign in ((0.0, 1.0), (20.0, -1.0)):                 # backward rays (w_z < 0)
+        bw = oracle.propagate(rays, zt, direction=oracle.BACKWARD)
+        assert (bw["dz"] < 0).all()
+        np.testing.assert_allclose(bw["ox"], sign * 10.0 * np.tan(th), rtol=1e-12)
+        # the moved origin lies on the original line: (o' - o) parallel to w
+        t = (zt - 10.0) / bw["dz"]
+        np.testing.assert_allclose(bw["ox"], t * dx, rtol=1e-12, atol=1e-15)
