@@ -158,4 +158,4 @@ def map_blob(cfg_name: str, path_id: int, seed: int = 1234) -> bytes:
     cfg = CONFIGS[cfg_name]
     nm = cfg.get("map_norm") or CONFIGS["C2"]["map_norm"]
     return R.make_map_blob(path_id, cfg["direction"], seed, nm["in_lo"], nm["in_hi"],
-                           nm["out_mid"], nm["out_half"])
+                           nm["out_mid"], nm["out_half"], plane_z=cfg["law"]["plane_z"])

@@ -165,10 +165,20 @@ def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     return u.astype(np.uint16)
 
 
-def write_map_blob(path_id: int, direction: int, in_lo, in_hi, out_mid, out_half, cls_layers, reg_layers) -> bytes:
+def _header(path_id: int, direction: int, ncl: int, nrl: int, plane_z) -> list:
+    """Magic + header; version 2 (with the f64 input plane z) when plane_z is given."""
+    if plane_z is None:
+        return [MAP_MAGIC, struct.pack("<IIQII", 1, int(direction), int(path_id), ncl, nrl)]
+    return [MAP_MAGIC, struct.pack("<IIQII", 2, int(direction), int(path_id), ncl, nrl),
+            struct.pack("<d", float(plane_z))]
+
+
+def write_map_blob(path_id: int, direction: int, in_lo, in_hi, out_mid, out_half, cls_layers, reg_layers,
+                   plane_z=None) -> bytes:
     """Serialise a factorised map from given layers [(W float32 (out, in), b float32 (out,)), ...];
-    W is rounded to bf16 (round-to-nearest-even).  Same layout as make_map_blob."""
-    parts = [MAP_MAGIC, struct.pack("<IIQII", 1, int(direction), int(path_id), len(cls_layers), len(reg_layers))]
+    W is rounded to bf16 (round-to-nearest-even).  Same layout as make_map_blob; plane_z (the
+    input plane of the training rays) makes a version-2 blob."""
+    parts = _header(path_id, direction, len(cls_layers), len(reg_layers), plane_z)
     for arr, n in ((in_lo, 4), (in_hi, 4), (out_mid, 6), (out_half, 6)):
         a = np.asarray(arr, dtype=np.float32)
         assert a.shape == (n,)
@@ -184,18 +194,18 @@ def write_map_blob(path_id: int, direction: int, in_lo, in_hi, out_mid, out_half
 
 
 def make_map_blob(path_id: int, direction: int, seed: int, in_lo, in_hi, out_mid, out_half,
-                  bias_range: float = 0.1) -> bytes:
+                  bias_range: float = 0.1, plane_z=None) -> bytes:
     """Serialise one path's factorised map (classifier + regressor) as a blob.
 
-    Layout (little-endian): magic 'PLTMAP01'; u32 version=1; u32 direction;
-    u64 path_id; u32 n_cls_layers; u32 n_reg_layers; f32 in_lo[4], in_hi[4],
+    Layout (little-endian): magic 'PLTMAP01'; u32 version (1, or 2 with plane_z); u32
+    direction; u64 path_id; u32 n_cls_layers; u32 n_reg_layers; [v2: f64 plane_z_mm, the
+    input plane the map was trained on]; f32 in_lo[4], in_hi[4],
     out_mid[6], out_half[6]; then for every layer (classifier first, then
     regressor): u32 out, u32 in, u16 W_bf16[out*in] (row-major, W[o][i]),
     f32 b[out].  Weights: Xavier-uniform gain 1, biases U(-bias_range, bias_range).
     """
     rng = np.random.default_rng([int(seed), int(path_id) & 0xFFFFFFFF, int(path_id) >> 32, 0xB10B])
-    parts = [MAP_MAGIC, struct.pack("<IIQII", 1, int(direction), int(path_id),
-                                    len(CLASSIFIER_DIMS) - 1, len(REGRESSOR_DIMS) - 1)]
+    parts = _header(path_id, direction, len(CLASSIFIER_DIMS) - 1, len(REGRESSOR_DIMS) - 1, plane_z)
     for arr, n in ((in_lo, 4), (in_hi, 4), (out_mid, 6), (out_half, 6)):
         a = np.asarray(arr, dtype=np.float32)
         assert a.shape == (n,)

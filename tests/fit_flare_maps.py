@@ -200,7 +200,8 @@ def main():
            "skipped": [pid for pid in ids if pid not in keep]}
     for p, pid in enumerate(keep):
         blob = R.write_map_blob(pid, cfg["direction"], lo[p].float().numpy(), hi[p].float().numpy(),
-                                ymid[p].float().numpy(), yhalf[p].float().numpy(), cls.layers(p), reg.layers(p))
+                                ymid[p].float().numpy(), yhalf[p].float().numpy(), cls.layers(p), reg.layers(p),
+                                plane_z=cfg["law"]["plane_z"])
         with open(os.path.join(a.out, a.config, f"{pid}.pltmap"), "wb") as f:
             f.write(blob)
     rep["seconds"] = time.time() - t0

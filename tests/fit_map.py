@@ -312,7 +312,8 @@ def main():
         return [(l.weight.detach().cpu().numpy(), l.bias.detach().cpu().numpy())
                 for l in m if isinstance(l, torch.nn.Linear)]
     blob = R.write_map_blob(pid, direction, lo.float().cpu().numpy(), hi.float().cpu().numpy(),
-                            ymid.float().cpu().numpy(), yhalf.float().cpu().numpy(), layers_of(cls), layers_of(reg))
+                            ymid.float().cpu().numpy(), yhalf.float().cpu().numpy(), layers_of(cls), layers_of(reg),
+                            plane_z=law["plane_z"])
     if a.out:
         os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
         with open(a.out, "wb") as f:

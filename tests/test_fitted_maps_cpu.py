@@ -17,12 +17,25 @@ MAPS = sorted(glob.glob(os.path.join(ROOT, "maps", "*.pltmap")))
 
 def test_writer_round_trips_a_parsed_blob():
     nm = C.CONFIGS["C2"]["map_norm"]
-    blob = R.make_map_blob(1024, 0, 77, nm["in_lo"], nm["in_hi"], nm["out_mid"], nm["out_half"])
-    p = oracle.parse_map_blob(blob)
-    layers = lambda h: [(W.astype(np.float32), b.astype(np.float32)) for W, b in zip(h["W"], h["b"])]
-    again = R.write_map_blob(p["path_id"], p["direction"], p["norm"][0:4], p["norm"][4:8], p["norm"][8:14],
-                             p["norm"][14:20], layers(p["classifier"]), layers(p["regressor"]))
-    assert again == blob
+    for plane in (None, -5.0):
+        blob = R.make_map_blob(1024, 0, 77, nm["in_lo"], nm["in_hi"], nm["out_mid"], nm["out_half"], plane_z=plane)
+        p = oracle.parse_map_blob(blob)
+        assert p["version"] == (1 if plane is None else 2) and p["plane_z"] == plane
+        layers = lambda h: [(W.astype(np.float32), b.astype(np.float32)) for W, b in zip(h["W"], h["b"])]
+        again = R.write_map_blob(p["path_id"], p["direction"], p["norm"][0:4], p["norm"][4:8], p["norm"][8:14],
+                                 p["norm"][14:20], layers(p["classifier"]), layers(p["regressor"]), plane_z=p["plane_z"])
+        assert again == blob
+
+
+def test_map_plane_is_enforced_by_oracle():
+    """Version-2 blobs record the input plane of their training rays: the
+    oracle's map query refuses rays on another plane (the library does too, plt.h)."""
+    blob = C.map_blob("C2", 1 << 10)
+    assert oracle.parse_map_blob(blob)["plane_z"] == -5.0
+    rays = R.gen_rays(C.CONFIGS["C2"]["law"], 3, 0, 64)
+    oracle.map_eval(blob, rays)
+    with pytest.raises(ValueError):
+        oracle.map_eval(blob, dict(rays, plane_z=-4.0))
 
 
 def test_writer_rounds_weights_to_nearest_bf16():
