@@ -375,6 +375,44 @@ PLT_API plt_status plt_shade_cards(const plt_scene_card* cards, int n_cards, dou
 PLT_API plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, plt_dir dir,
                                       int64_t n, void* cuda_stream);
 
+/*
+ * Synthetic input rays on the device (SURVEY.md §8(d) "Synthetic inputs": Philox4x32-10
+ * keyed by the seed, counted by the global ray index, so results are identical for any
+ * batch split or GPU count).  Writes rays [start, start + n) of the law into out's device
+ * arrays (n floats each; out->dz may be NULL: rays then carry (dx, dy) only, A32;
+ * out->plane_z_mm is not used -- the rays lie on law->plane_z_mm).  Specification (also
+ * implemented, independently, by plt_inputs/philox.py; the float32 rays are bit-identical):
+ * ray i draws u_0..u_7 = (x + 0.5) 2^-32 from the 8 words of Philox4x32-10 with counter
+ * (i mod 2^32, i div 2^32, b, 0x504C5452), b = 0, 1, key (seed mod 2^32, seed div 2^32),
+ * and maps them by the law below in IEEE double with one rounding per operation (the
+ * angle by an octant reduction and Taylor polynomials, plt_inputs/philox.py):
+ *   DISC_CAP    origin uniform on the disc (disc_r, centre (disc_x0, 0)), direction uniform
+ *               on the cap w_z >= cap_cos_min, lambda = lo + (hi - lo) u_4;
+ *   COLLIMATED  origin as DISC_CAP, direction (dir_x, 0, dir_z);
+ *   SENSOR_PUPIL origin uniform on the sensor_w x sensor_h rectangle, direction towards a
+ *               point uniform on the disc of radius pupil_r at z = pupil_z;
+ *   SENSOR_GRID as SENSOR_PUPIL with ray i in pixel i div spp of a width_px x height_px
+ *               grid (row-major, row 0 at +y).
+ * Errors: PLT_E_INVALID_ARG (null, bad kind, non-finite field, n < 0, start < 0, grid sizes
+ * <= 0), PLT_E_CUDA.
+ */
+typedef enum { PLT_LAW_DISC_CAP = 0, PLT_LAW_COLLIMATED = 1, PLT_LAW_SENSOR_PUPIL = 2, PLT_LAW_SENSOR_GRID = 3 } plt_law_kind;
+
+typedef struct {
+    int kind;                          /* plt_law_kind                                         */
+    int width_px, height_px, spp;      /* SENSOR_GRID                                          */
+    double plane_z_mm;                 /* plane of the ray origins                             */
+    double disc_r_mm, disc_x0_mm;      /* DISC_CAP, COLLIMATED: origin disc                    */
+    double cap_cos_min;                /* DISC_CAP: cos of the cap half-angle                  */
+    double dir_x, dir_z;               /* COLLIMATED: the fixed unit direction (x-z plane)     */
+    double sensor_w_mm, sensor_h_mm;   /* SENSOR_*: sensor rectangle centred on the axis       */
+    double pupil_z_mm, pupil_r_mm;     /* SENSOR_*: disc the directions aim at                 */
+    double lambda_lo_nm, lambda_hi_nm; /* lambda = lo + (hi - lo) u (lo == hi: one wavelength) */
+} plt_ray_law;
+
+PLT_API plt_status plt_gen_rays(const plt_ray_law* law, uint64_t seed, int64_t start, const plt_rays* out, int64_t n,
+                                void* cuda_stream);
+
 /* out[i] = film[i] * 2^-32 * scale (float), for channels*height*width pixels. */
 PLT_API plt_status plt_film_resolve(const plt_film_desc* film_desc, const int64_t* film, float* out,
                             double scale, void* cuda_stream);

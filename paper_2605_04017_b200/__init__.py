@@ -30,7 +30,7 @@ EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
             "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_shade_cards",
-            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel")
+            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays")
 
 
 class PltError(RuntimeError):
@@ -63,6 +63,17 @@ class FilmDesc(C.Structure):
 
 class ScenePlane(C.Structure):
     _fields_ = [("z_mm", C.c_double), ("period_mm", C.c_double), ("contrast", C.c_double)]
+
+
+class RayLaw(C.Structure):
+    _fields_ = [("kind", C.c_int), ("width_px", C.c_int), ("height_px", C.c_int), ("spp", C.c_int),
+                ("plane_z_mm", C.c_double), ("disc_r_mm", C.c_double), ("disc_x0_mm", C.c_double),
+                ("cap_cos_min", C.c_double), ("dir_x", C.c_double), ("dir_z", C.c_double),
+                ("sensor_w_mm", C.c_double), ("sensor_h_mm", C.c_double), ("pupil_z_mm", C.c_double),
+                ("pupil_r_mm", C.c_double), ("lambda_lo_nm", C.c_double), ("lambda_hi_nm", C.c_double)]
+
+
+LAW_KINDS = {"disc_cap": 0, "collimated": 1, "sensor_pupil": 2, "sensor_grid": 3}
 
 
 class SplatTarget(C.Structure):
@@ -105,11 +116,12 @@ def load():
     L.plt_shade_cards.argtypes = [p, i, d, d, p, i, i64, C.c_float, p, p, i64, p]
     L.plt_propagate_rays.argtypes = [p, p, d, i, i64, p]
     L.plt_trace_kernel.argtypes = [p, u64, i, i, p]
+    L.plt_gen_rays.argtypes = [p, u64, i64, p, i64, p]
     L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
               "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted",
-              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel"):
+              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -390,6 +402,34 @@ def propagate_rays(rays: dict, out: dict, z_target_mm: float, direction: int = F
     _check(load().plt_propagate_rays(C.byref(r), C.byref(o), float(z_target_mm), int(direction), n,
                                      _stream(stream)))
     out["plane_z"] = float(z_target_mm)
+
+
+def ray_law(k: dict) -> RayLaw:
+    """plt_ray_law from a dict of the law's DERIVED constants (kind, plane_z, lam_lo, lam_hi,
+    disc_r, disc_x0, cap_cos_min, dir_x, dir_z, sensor_w, sensor_h, pupil_z, pupil_r,
+    width_px, height_px, spp), e.g. plt_inputs.philox.law_constants(law)."""
+    g = lambda key: float(k.get(key, 0.0))
+    return RayLaw(LAW_KINDS[k["kind"]], int(k.get("width_px", 0)), int(k.get("height_px", 0)), int(k.get("spp", 0)),
+                  g("plane_z"), g("disc_r"), g("disc_x0"), g("cap_cos_min"), g("dir_x"), g("dir_z"), g("sensor_w"),
+                  g("sensor_h"), g("pupil_z"), g("pupil_r"), g("lam_lo"), g("lam_hi"))
+
+
+def gen_rays(law_constants: dict, seed: int, start: int, n: int, out: dict | None = None, with_dz: bool = True,
+             stream=None, device="cuda") -> dict:
+    """plt_gen_rays: rays [start, start + n) of a law, generated on the device (Philox4x32-10
+    keyed by seed, counted by the global index).  `out` (optional) holds preallocated arrays."""
+    import torch
+    n = int(n)
+    if out is None:
+        out = {k: torch.empty(n, dtype=torch.float32, device=device) for k in RAY_KEYS if with_dz or k != "dz"}
+        if not with_dz:
+            out["dz"] = None
+    out["plane_z"] = float(law_constants["plane_z"])
+    law = ray_law(law_constants)
+    r = _rays_struct(out, n)
+    _check(load().plt_gen_rays(C.byref(law), int(seed) & 0xFFFFFFFFFFFFFFFF, int(start), C.byref(r), n,
+                               _stream(stream)))
+    return out
 
 
 KERNEL_KINDS = {0: "jit", 1: "packed", 2: "scalar", 3: "fp64"}

@@ -384,6 +384,29 @@ plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_
     PLT_GUARD_END
 }
 
+plt_status plt_gen_rays(const plt_ray_law* law, uint64_t seed, int64_t start, const plt_rays* out, int64_t n,
+                        void* cuda_stream) {
+    PLT_RANGE("plt_gen_rays");
+    PLT_GUARD_BEGIN
+    if (!law || !out) return set_err(PLT_E_INVALID_ARG, "null law / out");
+    if (law->kind < PLT_LAW_DISC_CAP || law->kind > PLT_LAW_SENSOR_GRID) return set_err(PLT_E_INVALID_ARG, "bad law kind");
+    const double f[] = {law->plane_z_mm, law->disc_r_mm, law->disc_x0_mm, law->cap_cos_min, law->dir_x, law->dir_z,
+                        law->sensor_w_mm, law->sensor_h_mm, law->pupil_z_mm, law->pupil_r_mm, law->lambda_lo_nm,
+                        law->lambda_hi_nm};
+    for (double v : f)
+        if (!std::isfinite(v)) return set_err(PLT_E_INVALID_ARG, "non-finite ray-law field");
+    if (law->kind == PLT_LAW_SENSOR_GRID && (law->width_px <= 0 || law->height_px <= 0 || law->spp <= 0))
+        return set_err(PLT_E_INVALID_ARG, "sensor grid sizes must be > 0");
+    if (n < 0 || start < 0) return set_err(PLT_E_INVALID_ARG, "n and start must be >= 0");
+    if (n == 0) return PLT_OK;
+    if (!out->ox || !out->oy || !out->dx || !out->dy || !out->lambda_nm)
+        return set_err(PLT_E_INVALID_ARG, "null ray array");
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    return cuda_status(plt::launch_gen_rays(*law, seed, start, *out, n, cuda_stream), "gen_rays");
+    PLT_GUARD_END
+}
+
 plt_status plt_film_resolve(const plt_film_desc* fd, const int64_t* film, float* out, double scale, void* cuda_stream) {
     PLT_RANGE("plt_film_resolve");
     PLT_GUARD_BEGIN

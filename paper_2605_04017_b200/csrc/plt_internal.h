@@ -182,6 +182,8 @@ int launch_shade_cards(const SceneCards& sc, double z_hits, const plt_hits& hits
 int launch_propagate(const plt_rays& in, const plt_rays& out, float z_target, float sdir, int64_t n, void* stream);
 int launch_splat(const plt_film_desc& fd, int64_t* film, const plt_hits& hits, const uint8_t* channel,
                  float scale, int64_t n, unsigned long long* dropped, void* stream);
+int launch_gen_rays(const plt_ray_law& law, uint64_t seed, int64_t start, const plt_rays& out, int64_t n,
+                    void* stream);
 int launch_resolve(const plt_film_desc& fd, const int64_t* film, float* out, double scale, void* stream);
 int launch_eval_map(const void* d_weights, const MapLayout& lay, const MapParams& mp,
                     const plt_rays& in, const plt_hits& out, float* raw, int64_t n, void* stream,

@@ -47,14 +47,16 @@ CONFIGS = {
            "map_norm": {"in_lo": (0.0, -0.43, 0.0, 400.0), "in_hi": (13.23, 0.43, 0.43, 700.0),
                         "out_mid": (0.0, 0.0, 0.0, 0.0, 0.9, 0.5),
                         "out_half": (25.0, 25.0, 0.5, 0.5, 0.1, 0.5)}},
-    # C3 24 mm backward camera batch at 32768 spp scale (192x128 px x 32768 spp)
+    # C3 24 mm backward camera batch at 32768 spp scale (192x128 px x 32768 spp); C3 and C5
+    # draw their rays from the counter-based generator (plt_inputs/philox.py = plt_gen_rays
+    # on the device), so full-size batches are generated in HBM and sampled anywhere
     "C3": {"lens": "wide24", "direction": BACKWARD,
            "opts": lens_opts(sensor_z_mm=WIDE24_SENSOR_Z, sensor_w_mm=24.0, sensor_h_mm=16.0,
                              backward_exit_z_mm=-5.0),
            "seed": 3, "n": 192 * 128 * 32768,
            "law": {"kind": "sensor_pupil", "plane_z": WIDE24_SENSOR_Z, "sensor_w": 24.0,
                    "sensor_h": 16.0, "pupil_z": WIDE24_REAR_VERTEX_Z, "pupil_r": 9.8055,
-                   "lam": (400.0, 700.0)},
+                   "lam": (400.0, 700.0), "rng": "philox"},
            "map_norm": {"in_lo": (0.0, -0.8, 0.0, 400.0), "in_hi": (14.5, 0.8, 0.8, 700.0),
                         "out_mid": (0.0, 0.0, 0.0, 0.0, -0.8, 0.5),
                         "out_half": (30.0, 30.0, 0.8, 0.8, 0.2, 0.5)}},
@@ -91,7 +93,7 @@ CONFIGS = {
     "C5": {"lens": "dgauss50", "direction": FORWARD, "opts": lens_opts(), "seed": 5,
            "sizes": tuple(1 << k for k in range(20, 31, 2)),
            "law": {"kind": "disc_cap", "plane_z": -5.0, "disc_r": 1.05 * 12.6, "cap_deg": 25.0,
-                   "lam": (400.0, 700.0)}},
+                   "lam": (400.0, 700.0), "rng": "philox"}},
 }
 
 

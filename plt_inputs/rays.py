@@ -111,7 +111,12 @@ def gen_chunk(law: dict, seed: int, c: int, count: int = CHUNK) -> dict:
 
 
 def gen_rays(law: dict, seed: int, start: int, count: int) -> dict:
-    """Rays [start, start+count) of the global index range (chunk-aligned generation)."""
+    """Rays [start, start+count) of the global index range (chunk-aligned generation).
+    Laws with rng="philox" use the counter-based generator of plt_inputs/philox.py (the
+    one plt_gen_rays implements on the device) instead of numpy chunks."""
+    if law.get("rng") == "philox":
+        from . import philox
+        return philox.gen_rays(law, seed, start, max(0, count))
     if count <= 0:
         e = np.zeros(0, np.float32)
         return {k: e.copy() for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm")} | {"plane_z": float(law["plane_z"])}
@@ -137,6 +142,9 @@ def sample_indices(n_total: int, n_sample: int, seed: int) -> np.ndarray:
 
 def gen_rays_at(law: dict, seed: int, idx: np.ndarray) -> dict:
     """Rays at arbitrary global indices (regenerates the chunks that contain them)."""
+    if law.get("rng") == "philox":
+        from . import philox
+        return philox.rays_at(law, seed, idx)
     idx = np.asarray(idx, dtype=np.int64)
     out = {k: np.empty(idx.size, np.float32) for k in ("ox", "oy", "dx", "dy", "dz", "lambda_nm")}
     chunks = idx // CHUNK
