@@ -101,7 +101,9 @@ def trace(lens: OracleLens, path_id: int, direction: int, rays: dict, threads: i
     """Exact float64 trace of ``rays`` (float32 arrays widened) along ``path_id``.
 
     Returns valid (bool), px, py, dx, dy, dz, I (float64) in the ORIGINAL lens
-    frame and ``margins`` (n, 4) = (geometric edge mm, |kappa|, |disc| mm^2, |w_z|).
+    frame, ``margins`` (n, 4) = (geometric edge mm, |kappa|, |disc| mm^2, |w_z|) and
+    ``steps`` (n,) = surface steps begun (stop crossings included, +1 for the output
+    plane) before the ray terminated -- bookkeeping for the algorithmic work count.
     """
     S, L, zS, sgn = _frame(lens, direction)
     ox, oy, dx, dy, lam = (_f64(rays, k) for k in ("ox", "oy", "dx", "dy", "lambda_nm"))
@@ -115,6 +117,7 @@ def trace(lens: OracleLens, path_id: int, direction: int, rays: dict, threads: i
     valid = np.zeros(n, np.uint8)
     out = np.zeros((n, 6), np.float64)
     marg = np.zeros((n, 4), np.float64)
+    steps = np.zeros(n, np.int32)
     lib = _lib.lib()
     p = _lib.ptr
 
@@ -123,12 +126,12 @@ def trace(lens: OracleLens, path_id: int, direction: int, rays: dict, threads: i
             return
         lib.orc_trace(p(S), S.shape[0], p(L), int(path_id), hi - lo,
                       p(ox[lo:]), p(oy[lo:]), plane_z, p(dx[lo:]), p(dy[lo:]), p(dz[lo:]),
-                      p(lam[lo:]), p(valid[lo:]), p(out[lo:]), p(marg[lo:]))
+                      p(lam[lo:]), p(valid[lo:]), p(out[lo:]), p(marg[lo:]), p(steps[lo:]))
 
     _parallel(run, n, threads)
     res = {"valid": valid.astype(bool), "px": out[:, 0].copy(), "py": out[:, 1].copy(),
            "dx": out[:, 2].copy(), "dy": out[:, 3].copy(), "dz": out[:, 4].copy(),
-           "I": out[:, 5].copy(), "margins": marg}
+           "I": out[:, 5].copy(), "margins": marg, "steps": steps}
     if sgn < 0:
         res["dz"] = -res["dz"]
         res["dz"][~res["valid"]] = 0.0

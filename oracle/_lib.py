@@ -34,7 +34,7 @@ def lib():
         L.orc_glass_index.restype = d
         L.orc_glass_index.argtypes = [i, p, d]
         L.orc_trace.restype = None
-        L.orc_trace.argtypes = [p, i, p, u64, i64, p, p, d, p, p, p, p, p, p, p]
+        L.orc_trace.argtypes = [p, i, p, u64, i64, p, p, d, p, p, p, p, p, p, p, p]
         L.orc_mlp_forward.restype = None
         L.orc_mlp_forward.argtypes = [i, p, p, p, i64, p, p]
         L.orc_map_eval.restype = None

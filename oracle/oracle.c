@@ -95,7 +95,7 @@ static int asph_sag(const double* f, double c, double r2, double* sag, double* g
  */
 static int trace_one(const double* S, int n_surf, const double* L, uint64_t path_id,
                      double ox, double oy, double oz, double dx, double dy, double dz,
-                     double lambda, double out[6], double m[4])
+                     double lambda, double out[6], double m[4], int* steps)
 {
     /* O2 path decoding: K = floor(log2 id); interaction k is R <=> bit k-1 set. */
     int K = 63;
@@ -108,8 +108,12 @@ static int trace_one(const double* S, int n_surf, const double* L, uint64_t path
     int s = 0, dir = +1, k = 0;
     m[0] = INFINITY; m[1] = INFINITY; m[2] = INFINITY; m[3] = INFINITY;
 
-    /* O3 state machine: loop while the ray is inside the surface list. */
+    /* O3 state machine: loop while the ray is inside the surface list.  *steps counts the
+       surface steps begun (stop crossings included) plus 1 for the output plane, i.e. how
+       much of the path's work the ray needed before it terminated (bookkeeping only). */
+    *steps = 0;
     while (s >= 0 && s < n_surf) {
+        ++*steps;
         const double* f = S + (size_t)s * ORC_STRIDE;
         const double zs = f[0], R = f[1], a = f[2];
         const int is_stop = f[3] != 0.0;
@@ -243,6 +247,7 @@ static int trace_one(const double* S, int n_surf, const double* L, uint64_t path
     if (k != K) return 0;                  /* sequence not fully consumed */
 
     /* O8 output plane */
+    ++*steps;
     if (fabs(w[2]) < m[3]) m[3] = fabs(w[2]);
     if (!(w[2] > 0.0)) return 0;
     const double t = (L[1] - o[2]) / w[2];
@@ -264,12 +269,15 @@ static int trace_one(const double* S, int n_surf, const double* L, uint64_t path
 void orc_trace(const double* S, int n_surf, const double* L, uint64_t path_id,
                int64_t n, const double* ox, const double* oy, double plane_z,
                const double* dx, const double* dy, const double* dz, const double* lambda_nm,
-               uint8_t* valid, double* out /* n x 6 */, double* margins /* n x 4 */)
+               uint8_t* valid, double* out /* n x 6 */, double* margins /* n x 4 */,
+               int32_t* steps /* n, nullable: steps begun before termination */)
 {
     for (int64_t i = 0; i < n; ++i) {
         double o6[6] = {0, 0, 0, 0, 0, 0}, m4[4];
+        int st = 0;
         int v = trace_one(S, n_surf, L, path_id, ox[i], oy[i], plane_z,
-                          dx[i], dy[i], dz[i], lambda_nm[i], o6, m4);
+                          dx[i], dy[i], dz[i], lambda_nm[i], o6, m4, &st);
+        if (steps) steps[i] = st;
         valid[i] = (uint8_t)v;
         if (!v) memset(o6, 0, sizeof o6);
         memcpy(out + 6 * i, o6, sizeof o6);

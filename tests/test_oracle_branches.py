@@ -252,3 +252,17 @@ def test_band_excludes_few_rays_on_the_config_laws(name):
         t = oracle.trace(ol, pid, cfg["direction"], rays, threads=oracle.host_threads())
         k = int(near_edge(t["margins"]).sum())
         assert k <= max_excluded(rays["ox"].size), (name, pid, k)
+
+
+def test_steps_bookkeeping():
+    """`steps` counts the surface steps a ray began (stop crossings included) plus the output
+    plane: the basis of the algorithmic work count of the trace roofline."""
+    lens = oracle.load_lens(SLAB, {"sensor_z_mm": 12.0})
+    t = oracle.trace(lens, 1 << 2, 0, rays_of([0.0, 25.0], 0.0, 0.0, 0.0, 1.0, 550.0, Z_IN))
+    assert t["steps"].tolist() == [3, 1]                # through both faces + output; blocked at face 1
+    g = oracle.trace(lens, oracle.ghost_id(2, 2, 1), 0, rays_of(0.0, 0.0, 0.0, 0.0, 1.0, 550.0, Z_IN))
+    assert g["steps"].tolist() == [5]                   # T, R, R, T + output
+    from plt_inputs.lenses import LENSES
+    s = oracle.load_lens(LENSES["singlet"])             # stop at z = 0 (a = 8), two spherical faces
+    t = oracle.trace(s, 1 << 2, 0, rays_of([0.0, 9.0], 0.0, 0.0, 0.0, 1.0, 550.0, Z_IN))
+    assert t["steps"].tolist() == [4, 1]                # stop + 2 faces + output; blocked at the stop
