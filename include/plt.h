@@ -376,6 +376,29 @@ PLT_API plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, d
                                       int64_t n, void* cuda_stream);
 
 /*
+ * End-to-end query of a HOST-resident batch (the inference passage P:397-399 for rays that
+ * live in host memory): for chunks of `chunk` rays (a multiple of 32), the library copies
+ * the chunk's rays host -> device on its own copy stream, runs the exact trace (lens !=
+ * NULL) and/or the map (map != NULL) on `cuda_stream` with their valid hits splatted into
+ * splat->film (device, caller-owned, accumulated; splat may be NULL), and copies each
+ * chunk's hits back into host_trace / host_map (nullable: not returned).  Chunk c+1's
+ * copy overlaps chunk c's kernels (two device staging buffers from the library's pool,
+ * ordered by events); nothing synchronises the host.  film_host (nullable, n_film int64)
+ * receives the film after the last chunk.  The call returns once all work is enqueued: the
+ * host buffers must stay valid until cuda_stream has completed it, and should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for the copies to overlap.
+ * in: HOST SoA rays (dz may be NULL, A32); host_trace / host_map: HOST hit arrays
+ * (mask_bits ceil(n/32) words; flags ignored).  Same results as plt_trace_rays_splat /
+ * plt_eval_map_splat on the same rays (bit-identical hits and film).
+ * Errors: PLT_E_INVALID_ARG (null, chunk not a positive multiple of 32, neither lens nor
+ * map), the errors of the query calls, PLT_E_OOM, PLT_E_CUDA.
+ */
+PLT_API plt_status plt_query_host(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                                  const plt_map* map, const plt_rays* in, const plt_hits* host_trace,
+                                  const plt_hits* host_map, const plt_splat_target* splat, int64_t* film_host,
+                                  int64_t n, int64_t chunk, void* cuda_stream);
+
+/*
  * Synthetic input rays on the device (SURVEY.md §8(d) "Synthetic inputs": Philox4x32-10
  * keyed by the seed, counted by the global ray index, so results are identical for any
  * batch split or GPU count).  Writes rays [start, start + n) of the law into out's device

@@ -30,7 +30,7 @@ EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
             "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_shade_cards",
-            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays")
+            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays", "plt_query_host")
 
 
 class PltError(RuntimeError):
@@ -117,11 +117,13 @@ def load():
     L.plt_propagate_rays.argtypes = [p, p, d, i, i64, p]
     L.plt_trace_kernel.argtypes = [p, u64, i, i, p]
     L.plt_gen_rays.argtypes = [p, u64, i64, p, i64, p]
+    L.plt_query_host.argtypes = [p, u64, i, i, p, p, p, p, p, p, i64, i64, p]
     L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
               "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted",
-              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays"):
+              "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays",
+              "plt_query_host"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -430,6 +432,63 @@ def gen_rays(law_constants: dict, seed: int, start: int, n: int, out: dict | Non
     _check(load().plt_gen_rays(C.byref(law), int(seed) & 0xFFFFFFFFFFFFFFFF, int(start), C.byref(r), n,
                                _stream(stream)))
     return out
+
+
+def _host_ptr(t, n=None, dtype=None):
+    """Pointer to a contiguous CPU tensor (pinned for overlap) -- host side of plt_query_host."""
+    if t is None:
+        return None
+    if t.is_cuda:
+        raise ValueError("plt_query_host takes HOST tensors for rays / returned hits")
+    if not t.is_contiguous():
+        raise ValueError("host buffers must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"expected {dtype}, got {t.dtype}")
+    if n is not None and t.numel() < n:
+        raise ValueError(f"host buffer holds {t.numel()} < {n} elements")
+    return C.c_void_p(t.data_ptr())
+
+
+def alloc_host_hits(n: int, pin: bool = True) -> dict:
+    import torch
+    h = {k: torch.empty(n, dtype=torch.float32, pin_memory=pin) for k in HIT_KEYS}
+    h["mask_bits"] = torch.empty((n + 31) // 32, dtype=torch.int32, pin_memory=pin)
+    return h
+
+
+def query_host(lens, path_id: int, m, host_rays: dict, film_desc: dict | None = None, film=None, film_host=None,
+               host_trace: dict | None = None, host_map: dict | None = None, weight_scale: float = 1.0,
+               chunk: int = 1 << 21, direction: int = FORWARD, precision: int = FP32, channel=None,
+               n: int | None = None, stream=None):
+    """plt_query_host: trace (lens != None) and/or map (m != None) a batch whose rays are HOST
+    tensors (pinned), chunked host -> device copies on the library's copy stream overlapping
+    the kernels; hits optionally returned to host dicts (alloc_host_hits), valid hits
+    splatted into the device `film`, copied to `film_host` at the end."""
+    import torch
+    n = int(host_rays["ox"].numel()) if n is None else int(n)
+    f = torch.float32
+    r = Rays(*(_host_ptr(host_rays.get(k) if k == "dz" else host_rays[k], n, f) for k in RAY_KEYS),
+             float(host_rays["plane_z"]))
+
+    def hh(h):
+        if h is None:
+            return None
+        return Hits(_host_ptr(h["mask_bits"], (n + 31) // 32, torch.int32), *(_host_ptr(h[k], n, f) for k in HIT_KEYS),
+                    None)
+
+    ht, hm = hh(host_trace), hh(host_map)
+    spl, keep = (None, None)
+    if film is not None:
+        spl, keep = _splat_struct({"film_desc": film_desc, "film": film, "channel": channel,
+                                   "weight_scale": weight_scale}, n)
+    npx = film_desc["channels"] * film_desc["height_px"] * film_desc["width_px"] if film_desc else 0
+    _check(load().plt_query_host(lens.handle if lens is not None else None, int(path_id), int(direction),
+                                 int(precision), m.handle if m is not None else None, C.byref(r),
+                                 C.byref(ht) if ht is not None else None, C.byref(hm) if hm is not None else None,
+                                 C.byref(spl) if spl is not None else None,
+                                 _host_ptr(film_host, npx, torch.int64) if film_host is not None else None,
+                                 n, int(chunk), _stream(stream)))
+    return film_host
 
 
 KERNEL_KINDS = {0: "jit", 1: "packed", 2: "scalar", 3: "fp64"}

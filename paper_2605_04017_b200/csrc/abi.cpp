@@ -6,7 +6,9 @@
 // stream.  There is no CPU fallback.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
@@ -419,3 +421,149 @@ plt_status plt_film_resolve(const plt_film_desc* fd, const int64_t* film, float*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// plt_query_host: chunked host -> device -> query -> host pipeline (include/plt.h).
+// ---------------------------------------------------------------------------------------
+namespace {
+
+// One library-owned, non-blocking copy stream per device (created on first use).
+std::mutex g_copy_mu;
+std::vector<cudaStream_t> g_copy_streams;
+
+cudaError_t copy_stream(cudaStream_t* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(g_copy_mu);
+    if ((int)g_copy_streams.size() <= dev) g_copy_streams.resize(dev + 1, nullptr);
+    if (!g_copy_streams[dev]) {
+        e = cudaStreamCreateWithFlags(&g_copy_streams[dev], cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+    }
+    *out = g_copy_streams[dev];
+    return cudaSuccess;
+}
+
+struct EventPool {   // events destroyed when the call returns (destruction is deferred by CUDA)
+    std::vector<cudaEvent_t> ev;
+    cudaError_t make(int k) {
+        ev.resize(k, nullptr);
+        for (auto& x : ev) {
+            cudaError_t e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    ~EventPool() { for (auto x : ev) if (x) cudaEventDestroy(x); }
+};
+
+}  // namespace
+
+extern "C" plt_status plt_query_host(const plt_lens* lens, uint64_t path_id, plt_dir dir, plt_precision prec,
+                                     const plt_map* map, const plt_rays* in, const plt_hits* host_trace,
+                                     const plt_hits* host_map, const plt_splat_target* splat, int64_t* film_host,
+                                     int64_t n, int64_t chunk, void* cuda_stream) {
+    PLT_RANGE("plt_query_host");
+    PLT_GUARD_BEGIN
+    if (!lens && !map) return set_err(PLT_E_INVALID_ARG, "neither lens nor map given");
+    if (!rays_ok(in)) return set_err(PLT_E_INVALID_ARG, "null host ray pointer or non-finite plane z");
+    if (n < 0 || chunk <= 0 || chunk % 32) return set_err(PLT_E_INVALID_ARG, "n >= 0 and chunk a positive multiple of 32");
+    if (host_trace && !hits_ok(host_trace)) return set_err(PLT_E_INVALID_ARG, "null host_trace array");
+    if (host_map && !hits_ok(host_map)) return set_err(PLT_E_INVALID_ARG, "null host_map array");
+    if (film_host && (!splat || !splat->film || !splat->film_desc))
+        return set_err(PLT_E_INVALID_ARG, "film_host needs a splat target");
+    if (n == 0) return PLT_OK;
+    plt_status s = check_device();
+    if (s != PLT_OK) return s;
+    const int64_t C = chunk < n ? chunk : ((n + 31) / 32) * 32;
+    cudaStream_t cs = (cudaStream_t)cuda_stream, xs = nullptr;
+    cudaError_t e = copy_stream(&xs);
+    if (e != cudaSuccess) return cuda_status((int)e, "query_host copy stream");
+    const bool has_dz = in->dz != nullptr;
+    const int nin = has_dz ? 6 : 5;
+    const int nq = (lens ? 1 : 0) + (map ? 1 : 0);
+    // per staging slot: inputs, then per query 6 output arrays + mask words
+    const size_t words = (size_t)(C / 32);
+    const size_t slot_bytes = (size_t)C * 4 * nin + nq * ((size_t)C * 4 * 6 + words * 4);
+    plt::ScratchGuard stage(cuda_stream);
+    e = (cudaError_t)stage.alloc(2 * slot_bytes + 256);
+    if (e != cudaSuccess) return cuda_status((int)e, "query_host staging");
+    EventPool evs;
+    e = evs.make(5);   // [0,1] inputs of slot b copied, [2,3] slot b consumed (compute + D2H), [4] copies done
+    if (e != cudaSuccess) return cuda_status((int)e, "query_host events");
+    // the staging memory is free for the copy stream once earlier work on cs is done
+    e = cudaEventRecord(evs.ev[2], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(xs, evs.ev[2], 0);
+    if (e == cudaSuccess) e = cudaEventRecord(evs.ev[3], cs);
+    if (e != cudaSuccess) return cuda_status((int)e, "query_host ordering");
+    for (int64_t lo = 0, c = 0; lo < n; lo += C, ++c) {
+        const int64_t cn = (n - lo) < C ? (n - lo) : C;
+        const int b = (int)(c & 1);
+        char* base = (char*)stage.p + b * slot_bytes;
+        float* din[6];
+        for (int k = 0; k < nin; ++k) din[k] = (float*)(base + (size_t)k * C * 4);
+        const float* hin[6] = {in->ox, in->oy, in->dx, in->dy, has_dz ? in->dz : in->lambda_nm, in->lambda_nm};
+        // slot b is reusable once its previous chunk's kernels and D2H copies are done
+        e = cudaStreamWaitEvent(xs, evs.ev[2 + b], 0);
+        for (int k = 0; k < nin && e == cudaSuccess; ++k)
+            e = cudaMemcpyAsync(din[k], hin[k] + lo, (size_t)cn * 4, cudaMemcpyHostToDevice, xs);
+        if (e == cudaSuccess) e = cudaEventRecord(evs.ev[b], xs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, evs.ev[b], 0);
+        if (e != cudaSuccess) return cuda_status((int)e, "query_host H2D");
+        plt_rays dr{din[0], din[1], din[2], din[3], has_dz ? din[4] : nullptr, din[nin - 1], in->plane_z_mm};
+        char* ob = base + (size_t)C * 4 * nin;
+        plt_hits dh[2];
+        for (int q = 0; q < nq; ++q) {
+            char* o = ob + q * ((size_t)C * 4 * 6 + words * 4);
+            dh[q] = plt_hits{(uint32_t*)(o + (size_t)C * 4 * 6), (float*)o, (float*)(o + (size_t)C * 4),
+                             (float*)(o + (size_t)C * 8), (float*)(o + (size_t)C * 12), (float*)(o + (size_t)C * 16),
+                             (float*)(o + (size_t)C * 20), nullptr};
+        }
+        plt_splat_target st{};
+        if (splat) {   // the channel array (device, indexed like the rays) follows the chunk
+            st = *splat;
+            if (st.channel) st.channel += lo;
+        }
+        int q = 0;
+        if (lens) {
+            s = splat ? plt_trace_rays_splat(lens, path_id, dir, prec, &dr, &dh[q], &st, cn, cuda_stream)
+                      : plt_trace_rays(lens, path_id, dir, prec, &dr, &dh[q], cn, cuda_stream);
+            if (s != PLT_OK) return s;
+            ++q;
+        }
+        if (map) {
+            s = splat ? plt_eval_map_splat(map, &dr, &dh[q], nullptr, &st, cn, cuda_stream)
+                      : plt_eval_map(map, &dr, &dh[q], nullptr, cn, cuda_stream);
+            if (s != PLT_OK) return s;
+        }
+        // hits back to the host on the copy stream, after the kernels
+        e = cudaEventRecord(evs.ev[2 + b], cs);
+        bool d2h = false;
+        for (int k = 0; k < nq && e == cudaSuccess; ++k) {
+            const plt_hits* H = lens && k == 0 ? host_trace : host_map;
+            if (!H) continue;
+            if (!d2h) { e = cudaStreamWaitEvent(xs, evs.ev[2 + b], 0); d2h = true; }
+            float* const dst[6] = {H->px, H->py, H->dx, H->dy, H->dz, H->throughput};
+            float* const src[6] = {dh[k].px, dh[k].py, dh[k].dx, dh[k].dy, dh[k].dz, dh[k].throughput};
+            for (int a = 0; a < 6 && e == cudaSuccess; ++a)
+                e = cudaMemcpyAsync(dst[a] + lo, src[a], (size_t)cn * 4, cudaMemcpyDeviceToHost, xs);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(H->mask_bits + lo / 32, dh[k].mask_bits, (size_t)((cn + 31) / 32) * 4,
+                                    cudaMemcpyDeviceToHost, xs);
+        }
+        if (d2h && e == cudaSuccess) e = cudaEventRecord(evs.ev[2 + b], xs);   // slot free after the D2H too
+        if (e != cudaSuccess) return cuda_status((int)e, "query_host D2H");
+    }
+    // the caller's stream completes only after the last copies; then the staging is freed
+    e = cudaEventRecord(evs.ev[4], xs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, evs.ev[4], 0);
+    if (e == cudaSuccess && film_host) {
+        const plt_film_desc& fd = *splat->film_desc;
+        e = cudaMemcpyAsync(film_host, splat->film, (size_t)fd.channels * fd.height_px * fd.width_px * 8,
+                            cudaMemcpyDeviceToHost, cs);
+    }
+    if (e != cudaSuccess) return cuda_status((int)e, "query_host");
+    return cuda_status(stage.release(), "query_host staging");
+    PLT_GUARD_END
+}

@@ -89,11 +89,10 @@ def test_propagate_without_dz(gpu_lib):
             assert np.array_equal(out[k].cpu().numpy(), rays[k]), k
 
 
-def test_host_pipeline_without_dz(gpu_lib):
-    """query_host_batch moving 20 B per ray (no dz) gives the film of the device-resident
+def test_host_query_without_dz(gpu_lib):
+    """plt_query_host moving 20 B per ray (no dz) gives the film of the device-resident
     query on the same dz-less rays, bit for bit."""
     import torch
-    from paper_2605_04017_b200.pipeline import query_host_batch
     plt = gpu_lib
     cfg = C.CONFIGS["C2"]
     gl = plt.Lens(C.lens_text("C2"), **cfg["opts"])
@@ -103,12 +102,9 @@ def test_host_pipeline_without_dz(gpu_lib):
     fd = {"width_px": 256, "height_px": 128, "channels": 1, "sensor_w_mm": 36.0, "sensor_h_mm": 24.0}
     host = {k: torch.from_numpy(rays[k]).pin_memory() for k in plt.RAY_KEYS if k != "dz"}
     host["plane_z"] = rays["plane_z"]
-    d = {k: torch.empty(n, dtype=torch.float32, device="cuda") for k in plt.RAY_KEYS}
-    ht, hm = plt.alloc_hits(n), plt.alloc_hits(n)
     film = torch.zeros(256 * 128, dtype=torch.int64, device="cuda")
     fh = torch.empty_like(film, device="cpu").pin_memory()
-    query_host_batch(gl, gl.all_t_id(), m, host, d, ht, hm, fd, film, film_host=fh, weight_scale=1.0 / n,
-                     chunk=1 << 18)
+    plt.query_host(gl, gl.all_t_id(), m, host, fd, film, fh, weight_scale=1.0 / n, chunk=1 << 18)
     torch.cuda.synchronize()
     ref = torch.zeros_like(film)
     dd = plt.rays_to_device(rays, with_dz=False)
