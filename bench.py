@@ -4,8 +4,8 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl plt|reference]
 
 One STEP = one pass of the whole hot path over one batch of the
-C2 workload (BASELINE.json configs[1]: 50 mm double-Gauss, 2^24 rays per GPU,
-lambda uniform 400-700 nm, synthetic seeded rays):
+workload; by default the C2 workload (BASELINE.json configs[1]: 50 mm double-Gauss,
+2^24 rays per GPU, lambda uniform 400-700 nm, synthetic seeded rays):
   a8  enumerate_ghosts (host; lists the lens's transport paths)
   a6-a7 trace_rays  -- exact sequential all-T trace (fp32 + fp64 guard-band refine)
   a1-a5 eval_map    -- fused classifier-gated regressor (tcgen05/TMEM)
@@ -15,6 +15,14 @@ lambda uniform 400-700 nm, synthetic seeded rays):
   a10 film all-reduce over NCCL (N > 1)
 Every ray is queried both ways, so value = rays per step (all ranks) / step time.
 Scaling is weak: each rank owns its own chunk-aligned slice of the global index range.
+
+--config selects the other BASELINE.json workloads (SURVEY.md §8(e) partitioning):
+  C3     805,306,368 backward camera rays (192x128 px x 32768 spp), generated on the
+         device; strong scaling, each rank owns 128/N pixel rows; trace + map.
+  C4_22 / C4_59  flare image: every ghost x 3 channels x 2^20 rays, fp64 trace + per-ghost
+         map, splatted in-kernel; strong scaling over contiguous (ghost, channel, ray)
+         ranges, one NCCL int64 film all-reduce per image.
+  C5     the throughput sweep (--rays 2^20 .. 2^30 per GPU, device-generated), as C2.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the float64 CPU oracle
 (oracle/, test infrastructure) on the host cores over a bounded sample instead.
@@ -43,20 +51,6 @@ MAC_CLS, MAC_REG = 4 * 32 + 32 * 32 + 32, 4 * 32 + 4 * 32 * 32 + 32 * 6
 IO_BYTES_PER_RAY = 5 * 4 + 6 * 4 + 1.0 / 8        # SoA in (ox oy dx dy lambda) + SoA out + 1 mask bit
 MUFU_PER_CLK_PER_SM = 16                           # B200 nominal SFU rate (DESIGN.md roofline)
 FP32_LANES_PER_SM = 128                            # FFMA lanes per SM (DESIGN.md roofline)
-# Algorithmic FP32 FLOPs of the exact trace (counted from the O1-O8
-# formulas, add/mul/div/sqrt = 1 FLOP): per spherical interaction step 77, per stop 13,
-# output plane 6, input normalisation 9; weighted by the measured survival fraction at
-# each step of the C2 path (rays stop costing work once vignetted).
-TRACE_FLOPS_STEP, TRACE_FLOPS_STOP, TRACE_FLOPS_OUT, TRACE_FLOPS_INIT = 77, 13, 6, 9
-C2_ALIVE_BEFORE_STEP = (1.0, 0.837, 0.837, 0.781, 0.781, 0.738, 0.614, 0.561, 0.498, 0.441, 0.388)  # stop = 6th
-C2_ALIVE_AT_OUTPUT = 0.371
-
-
-def trace_flops_per_ray_c2() -> float:
-    f = TRACE_FLOPS_INIT + C2_ALIVE_AT_OUTPUT * TRACE_FLOPS_OUT
-    for k, a in enumerate(C2_ALIVE_BEFORE_STEP):
-        f += a * (TRACE_FLOPS_STOP if k == 5 else TRACE_FLOPS_STEP)
-    return f
 
 
 def load_peaks():
@@ -148,6 +142,9 @@ def dist_setup(args):
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         nccl = args.impl == "plt" and not share
+        if nccl:   # the communicator's init lines (rank count, NVLS/ring choice) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl" if nccl else "gloo",
                                 device_id=torch.device("cuda", local) if nccl else None)
     return ws, rank, local
@@ -253,7 +250,7 @@ def run_reference(args, ws, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": workload_config(args.rays, ws, pid),
+            "config": workload_config(args.rays or (1 << 24), ws, pid),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": f"each step = the first {n} rays of the C2 batch (bounded sample of the "
                                        f"2^24 rays per GPU of the GPU arm), float64 trace + map + splat"},
@@ -262,65 +259,25 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------------------------------
-def run_plt(args, ws, rank, local):
+CONFIGS = ("C2", "C3", "C4_22", "C4_59", "C5")
+FP64_LANES_PER_SM = 64                             # B200 FP64 FMA lanes per SM (nominal; DESIGN.md roofline)
+
+
+def trace_flops_table():
+    """profiles/trace_flops.json: algorithmic FLOPs per ray per (config, path), written by
+    tools/trace_flops.py from the oracle's step bookkeeping (a stored value; bench never runs
+    the oracle outside its cpu_baseline / reference legs)."""
+    with open(os.path.join(ROOT, "profiles", "trace_flops.json")) as f:
+        return json.load(f)["configs"]
+
+
+def timed_steps(step, args, dist, local, stream):
+    """W untimed steps, then K steps bracketed by barrier + synchronize and CUDA events on the
+    launching stream, NVML clocks sampled during the region.  Returns (seconds, clocks)."""
     import torch
-    import paper_2605_04017_b200 as plt
-    from plt_inputs import configs as C
-
-    plt.load()
-    fused = args.splat == "fused"
-    dev = torch.device("cuda", local)
-    n = args.rays
-    cfg, rays_np = make_workload(rank, n)
-    lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
-    pid = lens.all_t_id()
-    m = plt.Map(C.fitted_map_blob("C2"), lens=lens)
-    stream = torch.cuda.current_stream()
-
-    # inputs resident in HBM (device-timed value); pinned host copies for e2e
-    keys = [k for k in plt.RAY_KEYS if k in rays_np]
-    host = {k: torch.from_numpy(rays_np[k]).pin_memory() for k in keys}
-    d_rays = {k: host[k].to(dev) for k in keys}
-    d_rays["dz"] = None
-    d_rays["plane_z"] = rays_np["plane_z"]
-    h_trace = plt.alloc_hits(n, dev)
-    h_map = plt.alloc_hits(n, dev)
-    npx = FILM["channels"] * FILM["height_px"] * FILM["width_px"]
-    film = torch.zeros(npx, dtype=torch.int64, device=dev)
-    film_host = torch.empty(npx, dtype=torch.int64).pin_memory()
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    t_kern = {"trace_rays": 0.0, "eval_map": 0.0, "splat_sensor": 0.0, "film_allreduce": 0.0}
-
-    def step(ev=None):
-        lens.enumerate_ghosts(0)                       # a8 (host)
-        film.zero_()
-        if ev:
-            ev[0].record(stream)
-        spl = {"film_desc": FILM, "film": film, "weight_scale": 1.0 / n} if fused else None
-        plt.trace_rays(lens, pid, d_rays, h_trace, stream=stream, splat=spl)          # a6-a7 (+a9 fused)
-        if ev:
-            ev[1].record(stream)
-        plt.eval_map(m, d_rays, h_map, stream=stream, splat=spl)                      # a1-a5 (+a9 fused)
-        if ev:
-            ev[2].record(stream)
-        if not fused:
-            plt.splat_sensor(FILM, film, h_trace, weight_scale=1.0 / n, stream=stream)   # a9
-            plt.splat_sensor(FILM, film, h_map, weight_scale=1.0 / n, stream=stream)
-        if ev:
-            ev[3].record(stream)
-        if dist is not None:
-            dist.all_reduce(film)                                          # a10
-        if ev:
-            ev[4].record(stream)
-
     for _ in range(args.warmup):
-        step()
+        step(None)
     torch.cuda.synchronize()
-
     sampler = ClockSampler(local)
     sampler.start()
     if dist is not None:
@@ -331,121 +288,364 @@ def run_plt(args, ws, rank, local):
     sampler.mark_start()
     t0.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        step(k)
     t1.record(stream)
     torch.cuda.synchronize()
     sampler.mark_stop()
     if dist is not None:
         dist.barrier()
-    clocks = sampler.stop()
-    elapsed = t0.elapsed_time(t1) / 1e3
-    for ev in evs:   # per-kernel durations, CUDA events on the launching stream
-        t_kern["trace_rays"] += ev[0].elapsed_time(ev[1])
-        t_kern["eval_map"] += ev[1].elapsed_time(ev[2])
-        t_kern["splat_sensor"] += ev[2].elapsed_time(ev[3])
-        t_kern["film_allreduce"] += ev[3].elapsed_time(ev[4])
+    return t0.elapsed_time(t1) / 1e3, sampler.stop()
+
+
+class Events:
+    """Per-kernel-group durations inside the timed steps (CUDA events on the launching stream)."""
+
+    def __init__(self, names, steps, stream):
+        import torch
+        self.names, self.stream = names, stream
+        self.ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(steps)]
+
+    def mark(self, k, i):
+        if k is not None:
+            self.ev[k][i].record(self.stream)
+
+    def per_step_ms(self):
+        out = {n: 0.0 for n in self.names}
+        for ev in self.ev:
+            for i, n in enumerate(self.names):
+                out[n] += ev[i].elapsed_time(ev[i + 1])
+        return {n: v / len(self.ev) for n, v in out.items()}
+
+
+def mask_valid_frac(h, n):
+    w = h["mask_bits"][: (n + 31) // 32].cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(w.view(np.uint8), bitorder="little")[:n]
+    return float(bits.sum()) / max(n, 1)
+
+
+def map_roofline(rays, v, secs, sm_max):
+    """eval_map: MUFU tanh roofline -- 64 classifier + 160 regressor tanh per valid ray."""
+    tanh = rays * (TANH_PER_RAY_CLS + TANH_PER_RAY_REG * v)
+    peak = MUFU_PER_CLK_PER_SM * 148 * sm_max * 1e6 / 1e9
+    ach = tanh / secs / 1e9
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Gtanh/s", "frac": ach / peak,
+            "peak_source": "16 MUFU/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md)", "tanh_per_ray": tanh / rays}
+
+
+def trace_roofline(flops, secs, sm_max, fp64=False):
+    """trace_rays: algorithmic FLOPs (profiles/trace_flops.json) against the FP32 (or FP64) peak."""
+    lanes = FP64_LANES_PER_SM if fp64 else FP32_LANES_PER_SM
+    peak = lanes * 2 * 148 * sm_max * 1e6 / 1e12
+    ach = flops / secs / 1e12
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "peak_source": f"{lanes} {'FP64' if fp64 else 'FP32'} lanes x 2 x 148 SMs x sm_max_mhz (DESIGN.md)"}
+
+
+def run_plt(args, ws, rank, local):
+    import torch
+    import paper_2605_04017_b200 as plt
+    from plt_inputs import configs as C
+    from plt_inputs import philox as PX
+
+    plt.load()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+    peaks, peaks_src = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    flops_tab = trace_flops_table()
+    name = args.config
+    fused = args.splat == "fused"
+    e2e = None
+    extra_cfg = {}
+    cpu_base = None
+
+    if name in ("C2", "C5"):
+        # ---- batch workloads (weak scaling): every ray traced + mapped + splatted ----------
+        n = args.rays if args.rays else (1 << 24 if name == "C2" else max(C.CONFIGS["C5"]["sizes"]))
+        cfg = C.CONFIGS[name]
+        lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+        pid = lens.all_t_id()
+        m = plt.Map(C.fitted_map_blob("C2"), lens=lens)           # C5 = the C2 lens, law and plane
+        if name == "C2":
+            _, rays_np = make_workload(rank, n)
+            keys = [k for k in plt.RAY_KEYS if k in rays_np]
+            host = {k: torch.from_numpy(rays_np[k]).pin_memory() for k in keys}
+            d_rays = {k: host[k].to(dev) for k in keys}
+            d_rays["dz"] = None
+            d_rays["plane_z"] = rays_np["plane_z"]
+        else:   # device-generated (Philox), the rank's slice of the global index range
+            d_rays = plt.gen_rays(PX.law_constants(cfg["law"]), cfg["seed"], rank * n, n, with_dz=False)
+        h_trace, h_map = plt.alloc_hits(n, dev), plt.alloc_hits(n, dev)
+        npx = FILM["channels"] * FILM["height_px"] * FILM["width_px"]
+        film = torch.zeros(npx, dtype=torch.int64, device=dev)
+        ev = Events(["trace_rays", "eval_map", "splat_sensor", "film_allreduce"], args.steps, stream)
+
+        def step(k):
+            lens.enumerate_ghosts(0)                                   # a8 (host)
+            film.zero_()
+            ev.mark(k, 0)
+            spl = {"film_desc": FILM, "film": film, "weight_scale": 1.0 / n} if fused else None
+            plt.trace_rays(lens, pid, d_rays, h_trace, stream=stream, splat=spl)        # a6-a7 (+a9)
+            ev.mark(k, 1)
+            plt.eval_map(m, d_rays, h_map, stream=stream, splat=spl)                    # a1-a5 (+a9)
+            ev.mark(k, 2)
+            if not fused:
+                plt.splat_sensor(FILM, film, h_trace, weight_scale=1.0 / n, stream=stream)   # a9
+                plt.splat_sensor(FILM, film, h_map, weight_scale=1.0 / n, stream=stream)
+            ev.mark(k, 3)
+            if dist is not None:
+                dist.all_reduce(film)                                  # a10
+            ev.mark(k, 4)
+
+        elapsed, clocks = timed_steps(step, args, dist, local, stream)
+        if name == "C2":
+            e2e = e2e_query_host(args, plt, lens, pid, m, host, rays_np["plane_z"], film, n, dist, stream, dev)
+        v_map, v_trace = mask_valid_frac(h_map, n), mask_valid_frac(h_trace, n)
+        per = {k: v / 1e3 for k, v in ev.per_step_ms().items()}
+        fl = flops_tab[name][str(pid)]["flops_per_ray"]
+        kernels = {
+            "trace_rays": {"ms": per["trace_rays"] * 1e3, "M_rays_s": n / per["trace_rays"] / 1e6, "valid_frac": v_trace,
+                           "kernel": plt.trace_kernel(lens, pid),
+                           "roofline": dict(trace_roofline(n * fl, per["trace_rays"], sm_max), flops_per_ray=fl),
+                           "hbm_GBs": n * IO_BYTES_PER_RAY / per["trace_rays"] / 1e9},
+            "eval_map": {"ms": per["eval_map"] * 1e3, "M_rays_s": n / per["eval_map"] / 1e6, "valid_frac": v_map,
+                         "roofline": map_roofline(n, v_map, per["eval_map"], sm_max),
+                         "tensor_frac": 2.0 * n * (MAC_CLS + MAC_REG * v_map) / per["eval_map"] / 1e12
+                         / float(peaks["bf16_tflops"]),
+                         "hbm_GBs": n * IO_BYTES_PER_RAY / per["eval_map"] / 1e9},
+            "splat_sensor": {"ms": per["splat_sensor"] * 1e3,
+                             "mode": "fused into trace_rays / eval_map epilogues" if fused else "separate kernel"},
+            "film_allreduce": {"ms": per["film_allreduce"] * 1e3},
+        }
+        rays_per_rank, scaling, launches = n, "weak", 3 if fused else 5
+        dtype = "f32 trace (+f64 refine), bf16xbf16->f32 map"
+        if name == "C2":
+            cfg_line = workload_config(n, ws, pid)
+        else:
+            size = f"2^{n.bit_length() - 1}" if n & (n - 1) == 0 else str(n)
+            cfg_line = {"workload": f"C5: throughput sweep point, C2 lens and law, {size} rays per GPU generated on "
+                                    "the device (plt_gen_rays, Philox keyed by global index), all-T trace + fitted map"
+                                    " + fused splat" + (" + NCCL film all-reduce" if ws > 1 else ""),
+                        "rays_per_gpu": n, "lens": "dgauss50", "path_id": pid,
+                        "l2": f"inputs {20 * n / 1e6:.0f} MB/GPU" + (" > 126 MB L2" if 20 * n > 126e6 else " (fit in L2)"),
+                        "parallelism": f"dp{ws} over rays"}
+        if ws == 1 and not args.no_cpu_baseline and name == "C2":
+            cpu_base = cpu_baseline()
+    elif name == "C3":
+        # ---- backward camera batch at the 32768-spp scale (strong scaling by pixel rows) ----
+        cfg = C.CONFIGS[name]
+        total = cfg["n"]
+        rows = 128
+        if rows % ws:
+            raise SystemExit("C3 shards 128 pixel rows: world size must divide 128")
+        n = total // ws                                   # rows/ws pixel rows x 192 px x 32768 spp
+        lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+        pid = lens.all_t_id()
+        m = plt.Map(C.fitted_map_blob("C3"), lens=lens)
+        d_rays = plt.gen_rays(PX.law_constants(cfg["law"]), cfg["seed"], rank * n, n, with_dz=False)
+        h_trace, h_map = plt.alloc_hits(n, dev), plt.alloc_hits(n, dev)
+        ev = Events(["trace_rays", "eval_map"], args.steps, stream)
+
+        def step(k):
+            ev.mark(k, 0)
+            plt.trace_rays(lens, pid, d_rays, h_trace, direction=plt.BACKWARD, stream=stream)
+            ev.mark(k, 1)
+            plt.eval_map(m, d_rays, h_map, stream=stream)
+            ev.mark(k, 2)
+
+        elapsed, clocks = timed_steps(step, args, dist, local, stream)
+        v_map, v_trace = mask_valid_frac(h_map, n), mask_valid_frac(h_trace, n)
+        per = {k: v / 1e3 for k, v in ev.per_step_ms().items()}
+        fl = flops_tab[name][str(pid)]["flops_per_ray"]
+        kernels = {
+            "trace_rays": {"ms": per["trace_rays"] * 1e3, "M_rays_s": n / per["trace_rays"] / 1e6, "valid_frac": v_trace,
+                           "kernel": plt.trace_kernel(lens, pid, plt.BACKWARD),
+                           "roofline": dict(trace_roofline(n * fl, per["trace_rays"], sm_max), flops_per_ray=fl)},
+            "eval_map": {"ms": per["eval_map"] * 1e3, "M_rays_s": n / per["eval_map"] / 1e6, "valid_frac": v_map,
+                         "roofline": map_roofline(n, v_map, per["eval_map"], sm_max)},
+        }
+        rays_per_rank, scaling, launches = n, "strong", 3
+        dtype = "f32 trace (+f64 refine), bf16xbf16->f32 map"
+        cfg_line = {"workload": "C3: 24 mm wide-angle (Nakamura x1.0897 stand-in), backward camera batch at the "
+                                "32768-spp scale: 192x128 px x 32768 spp = 805,306,368 rays generated on the device "
+                                "(plt_gen_rays), all-T backward trace + fitted backward map (maps/C3_0.pltmap)",
+                    "rays_total": total, "rays_per_gpu": n, "lens": "wide24", "path_id": pid,
+                    "l2": f"inputs {20 * n / 1e9:.1f} GB/GPU > 126 MB L2",
+                    "parallelism": f"{ws} ranks x {rows // ws} pixel rows (strong scaling)"}
+    else:
+        # ---- flare image: every two-bounce ghost x 3 channels x 2^20 rays (strong scaling over
+        # (ghost, channel, ray) ranges), fp64 trace + per-ghost map, both splatted in-kernel,
+        # one NCCL int64 film all-reduce per image (Eq. 8, P:250-257) --------------------------
+        cfg = C.CONFIGS[name]
+        lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+        ids, _ = lens.enumerate_ghosts(2)
+        ghosts = [int(g) for g in ids[1:]]
+        npc = cfg["n_per_channel"]
+        fd = cfg["film"]
+        maps, fitted = {}, 0
+        for g in ghosts:
+            path = os.path.join(ROOT, "maps", "flare", name, f"{g}.pltmap")
+            if os.path.exists(path):
+                maps[g] = plt.Map(open(path, "rb").read(), lens=lens)
+                fitted += 1
+            else:   # the few paths too rare to fit (maps/README.md): seeded weights
+                maps[g] = plt.Map(C.map_blob(name, g, seed=g % 100000), lens=lens)
+        K = {c: PX.law_constants(dict(cfg["law"], lam=lam)) for c, lam in enumerate(cfg["channels"])}
+        chans = [plt.gen_rays(K[c], cfg["seed"] * 16 + c, 0, npc) for c in range(3)]
+        chan_ids = [torch.full((npc,), c, dtype=torch.uint8, device=dev) for c in range(3)]
+        total = len(ghosts) * 3 * npc
+        lo_q, hi_q = rank * total // ws, (rank + 1) * total // ws
+        segs = []            # (ghost, channel, first ray, count) of this rank's flat range
+        q = lo_q
+        while q < hi_q:
+            item, i0 = divmod(q, npc)
+            g, c = ghosts[item // 3], item % 3
+            cnt = min(npc - i0, hi_q - q)
+            segs.append((g, c, i0, cnt))
+            q += cnt
+        h = plt.alloc_hits(npc, dev)
+        film = torch.zeros(fd["channels"] * fd["height_px"] * fd["width_px"], dtype=torch.int64, device=dev)
+        ev = Events(["trace_rays", "eval_map", "film_allreduce"], args.steps, stream)
+
+        def view(d, i0, cnt):
+            return {k: (v[i0:i0 + cnt] if k != "plane_z" and v is not None else v) for k, v in d.items()}
+
+        def step(k):
+            film.zero_()
+            ev.mark(k, 0)
+            for g, c, i0, cnt in segs:
+                spl = {"film_desc": fd, "film": film, "channel": chan_ids[c][i0:i0 + cnt], "weight_scale": 1.0 / npc}
+                plt.trace_rays(lens, g, view(chans[c], i0, cnt), h, precision=plt.FP64, n=cnt, stream=stream,
+                               splat=spl)
+            ev.mark(k, 1)
+            for g, c, i0, cnt in segs:
+                spl = {"film_desc": fd, "film": film, "channel": chan_ids[c][i0:i0 + cnt], "weight_scale": 1.0 / npc}
+                plt.eval_map(maps[g], view(chans[c], i0, cnt), h, n=cnt, stream=stream, splat=spl)
+            ev.mark(k, 2)
+            if dist is not None:
+                dist.all_reduce(film)
+            ev.mark(k, 3)
+
+        elapsed, clocks = timed_steps(step, args, dist, local, stream)
+        if args.dump_film and rank == 0:
+            np.save(args.dump_film, film.cpu().numpy())
+        per = {k: v / 1e3 for k, v in ev.per_step_ms().items()}
+        n = hi_q - lo_q
+        fl = sum(flops_tab[name][str(g)]["flops_per_ray"] * cnt for g, c, i0, cnt in segs)
+        # valid fraction of this rank's map queries (for the tanh count): re-run outside the timing
+        vm_rays = 0
+        for g, c, i0, cnt in segs:
+            plt.eval_map(maps[g], view(chans[c], i0, cnt), h, n=cnt, stream=stream)
+            vm_rays += mask_valid_frac(h, cnt) * cnt
+        v_map = vm_rays / max(n, 1)
+        kernels = {
+            "trace_rays": {"ms": per["trace_rays"] * 1e3, "M_rays_s": n / per["trace_rays"] / 1e6,
+                           "precision": "fp64 (binding for ghosts, A22)",
+                           "roofline": dict(trace_roofline(fl, per["trace_rays"], sm_max, fp64=True),
+                                            flops_per_ray=fl / max(n, 1))},
+            "eval_map": {"ms": per["eval_map"] * 1e3, "M_rays_s": n / per["eval_map"] / 1e6, "valid_frac": v_map,
+                         "roofline": map_roofline(n, v_map, per["eval_map"], sm_max)},
+            "film_allreduce": {"ms": per["film_allreduce"] * 1e3, "bytes": film.numel() * 8},
+        }
+        rays_per_rank, scaling, launches = n, "strong", 2 * len(segs)
+        dtype = "f64 trace, bf16xbf16->f32 map"
+        cfg_line = {"workload": f"{name}: {'22 mm Nakamura @15 deg' if name == 'C4_22' else '59 mm double-Gauss @10 deg'} "
+                                f"flare image, {len(ghosts)} two-bounce ghosts x 3 channels x 2^20 rays "
+                                f"= {total:,} queries, each traced (fp64) and mapped ({fitted} fitted per-ghost maps, "
+                                f"{len(ghosts) - fitted} seeded), splatted in-kernel into a 768x512x3 int64 film"
+                                + (", one NCCL film all-reduce per image" if ws > 1 else ""),
+                    "rays_total": total, "rays_per_gpu": n, "lens": cfg["lens"], "ghosts": len(ghosts),
+                    "l2": "rays 3 x 2^20 x 24 B = 75 MB, re-read per ghost (L2-resident by design)",
+                    "parallelism": f"{ws} ranks x contiguous (ghost, channel, ray) ranges (strong scaling)"}
+        extra_cfg["segments_rank0"] = len(segs)
+
+    # ---- one JSON line (max over ranks) ------------------------------------------------------
     step_s = elapsed / args.steps
+    vals = torch.tensor([step_s, e2e["s"] if e2e else 0.0], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    step_s, e2e_s = vals.tolist()
+    if rank != 0:
+        return
+    dominant = max((k for k in kernels if "roofline" in kernels[k]), key=lambda k: kernels[k]["ms"])
+    roof = dict(kernels[dominant]["roofline"])
+    roof["kernel"] = dominant
+    roof["traffic"] = ncu_traffic(dominant) if name == "C2" else None
+    rays_all = rays_per_rank * ws if scaling == "weak" else (cfg_line.get("rays_total") or rays_per_rank * ws)
+    line = {
+        "metric": METRIC, "value": rays_all / step_s / 1e6, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": dict(cfg_line, name=name, **extra_cfg),
+        "roofline": roof,
+        "kernels": kernels,
+        "e2e": ({"value": rays_all / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
+                 "d2h_bytes_per_step": e2e["d2h"], "path": "plt_query_host (C-ABI, host buffers)",
+                 "h2d_GBs": e2e["h2d"] / e2e_s / 1e9, "pinned_h2d_GBs_measured": e2e["h2d_peak"],
+                 "frac_of_pinned_h2d": e2e["h2d"] / e2e_s / 1e9 / e2e["h2d_peak"]} if e2e else
+                {"value": None, "note": "inputs are generated on the device for this config (plt_gen_rays)"}),
+        "gpu_launches": args.steps * launches,
+        "clocks": clocks,
+        "peaks_source": peaks_src,
+    }
+    if cpu_base is not None:
+        line["cpu_baseline"] = cpu_base
+    print(json.dumps(line), flush=True)
 
-    # ---------------- e2e: host buffers -> device -> step -> film back to host ----------
-    e2e_steps = max(3, min(args.steps, 10))
 
-    from paper_2605_04017_b200.pipeline import query_host_batch
-    host_rays = dict(host, plane_z=rays_np["plane_z"])
-    copy_stream = torch.cuda.Stream(device=dev)
-    chunk = args.e2e_chunk
-    copy_done = [torch.cuda.Event() for _ in range((n + chunk - 1) // chunk)]
+def pinned_h2d_gbs(dev, nbytes=1 << 30):
+    """Measured host->device bandwidth from pinned memory (one 1 GiB copy, best of 3)."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+    return best
+
+
+def e2e_query_host(args, plt, lens, pid, m, host, plane_z, film, n, dist, stream, dev):
+    """The same step end to end through the C-ABI host-buffer call plt_query_host: the rays'
+    host -> device copies (chunked, on the library's copy stream, overlapping the kernels),
+    trace + map + fused splat, and the film back to pinned host memory, every step."""
+    import torch
+    fused = args.splat == "fused"
+    host_rays = dict(host, plane_z=plane_z)
+    film_host = torch.empty(film.numel(), dtype=torch.int64).pin_memory()
+    steps = max(3, min(args.steps, 10))
 
     def e2e_step():
-        # the public host-batch path: chunked H2D on a copy stream overlapping the kernels
         lens.enumerate_ghosts(0)
         film.zero_()
-        query_host_batch(lens, pid, m, host_rays, d_rays, h_trace, h_map, FILM, film, None,
-                         weight_scale=1.0 / n, chunk=chunk, compute_stream=stream, copy_stream=copy_stream,
-                         copy_done=copy_done, fused=fused)
+        plt.query_host(lens, pid, m, host_rays, FILM, film, None if dist is not None else film_host,
+                       weight_scale=1.0 / n, chunk=args.e2e_chunk, stream=stream)
         if dist is not None:
             dist.all_reduce(film)
-        film_host.copy_(film, non_blocking=True)
+            film_host.copy_(film, non_blocking=True)
 
+    if not fused:
+        return None
     e2e_step()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(e2e_steps):
+    for _ in range(steps):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_s = e0.elapsed_time(e1) / 1e3 / e2e_steps
-
-    # valid fractions (for the algorithmic tanh count) -- outside the timed region
-    def valid_frac(h):
-        w = h["mask_bits"].cpu().numpy().view(np.uint32)
-        return float(np.unpackbits(w.view(np.uint8)).sum()) / n
-
-    v_map, v_trace = valid_frac(h_map), valid_frac(h_trace)
-
-    vals = torch.tensor([step_s, e2e_s, elapsed], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    step_s, e2e_s, elapsed = vals.tolist()
-    if rank != 0:
-        return
-
-    peaks, peaks_src = load_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    per_step = {k: v / args.steps / 1e3 for k, v in t_kern.items()}
-    # eval_map roofline: MUFU (tanh) bound; algorithmic tanh = 64 per ray + 160 per valid ray
-    tanh_per_launch = n * (TANH_PER_RAY_CLS + TANH_PER_RAY_REG * v_map)
-    mufu_peak = MUFU_PER_CLK_PER_SM * 148 * sm_max * 1e6 / 1e9       # G tanh/s
-    map_ach = tanh_per_launch / per_step["eval_map"] / 1e9
-    flops_map = 2.0 * n * (MAC_CLS + MAC_REG * v_map)
-    fp32_peak = FP32_LANES_PER_SM * 2 * 148 * sm_max * 1e6 / 1e12         # TFLOP/s
-    trace_tflops = n * trace_flops_per_ray_c2() / per_step["trace_rays"] / 1e12
-    trace_bytes = n * IO_BYTES_PER_RAY
-    kernels = {
-        "eval_map": {"ms": per_step["eval_map"] * 1e3, "M_rays_s": n / per_step["eval_map"] / 1e6,
-                     "valid_frac": v_map,
-                     "roofline": {"bound": "alu", "achieved": map_ach, "peak": mufu_peak, "unit": "Gtanh/s",
-                                  "frac": map_ach / mufu_peak,
-                                  "peak_source": "16 MUFU/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md)"},
-                     "tensor_TFLOPs": flops_map / per_step["eval_map"] / 1e12,
-                     "tensor_frac": flops_map / per_step["eval_map"] / 1e12 / float(peaks["bf16_tflops"]),
-                     "hbm_GBs": trace_bytes / per_step["eval_map"] / 1e9},
-        "trace_rays": {"ms": per_step["trace_rays"] * 1e3, "M_rays_s": n / per_step["trace_rays"] / 1e6,
-                       "valid_frac": v_trace,
-                       "roofline": {"bound": "alu", "achieved": trace_tflops, "peak": fp32_peak,
-                                    "unit": "TFLOP/s", "frac": trace_tflops / fp32_peak,
-                                    "peak_source": "128 FP32 lanes x 2 x 148 SMs x sm_max_mhz (DESIGN.md)",
-                                    "flops_per_ray": trace_flops_per_ray_c2()},
-                       "hbm_GBs": trace_bytes / per_step["trace_rays"] / 1e9,
-                       "hbm_frac": trace_bytes / per_step["trace_rays"] / 1e9 / float(peaks["hbm_gbs"])},
-        "splat_sensor": {"ms": per_step["splat_sensor"] * 1e3,
-                         "mode": "fused into trace_rays / eval_map epilogues" if fused else "separate kernel"},
-        "film_allreduce": {"ms": per_step["film_allreduce"] * 1e3},
-    }
-    dominant = max(("eval_map", "trace_rays"), key=lambda k: kernels[k]["ms"])
-    roof = dict(kernels[dominant]["roofline"])
-    roof["kernel"] = dominant
-    roof["traffic"] = ncu_traffic(dominant)
-    value = ws * n / step_s / 1e6
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 trace (+f64 refine), bf16xbf16->f32 map", "data": "synthetic",
-        "config": workload_config(n, ws, pid),
-        "roofline": roof,
-        "kernels": kernels,
-        "e2e": {"value": ws * n / e2e_s / 1e6, "unit": UNIT,
-                "h2d_bytes_per_step": 4 * len(keys) * n, "d2h_bytes_per_step": npx * 8},
-        "gpu_launches": args.steps * (3 if fused else 5),
-        "clocks": clocks,
-        "peaks_source": peaks_src,
-    }
-    if ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline()
-    print(json.dumps(line), flush=True)
+    h2d = sum(int(v.numel()) * 4 for k, v in host.items() if k != "plane_z")
+    return {"s": e0.elapsed_time(e1) / 1e3 / steps, "h2d": h2d, "d2h": film.numel() * 8,
+            "h2d_peak": pinned_h2d_gbs(dev)}
 
 
 def main():
@@ -454,7 +654,10 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["plt", "reference"], default="plt")
-    ap.add_argument("--rays", type=int, default=1 << 24, help="rays per GPU per step")
+    ap.add_argument("--config", choices=CONFIGS, default="C2",
+                    help="BASELINE.json workload: C2 (default, the N=1 headline), C3, C4_22, C4_59, C5")
+    ap.add_argument("--rays", type=int, default=0, help="rays per GPU per step (C2: 2^24, C5: 2^30 by default)")
+    ap.add_argument("--dump-film", default=None, help="(C4) save rank 0's final film (.npy) -- for tests")
     ap.add_argument("--ref-rays", type=int, default=1 << 15, help="rays per oracle step (--impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="rays per H2D chunk of the e2e leg")

@@ -1,13 +1,14 @@
-"""Per-configuration throughput of the CUDA path on one B200 (BASELINE.json configs C1-C5).
+"""Per-configuration throughput and roofline fractions of the CUDA path on one B200
+(BASELINE.json configs C1-C5).
 
-    python tools/configs_bench.py [--out profiles/r01_configs.json] [--quick]
+    python tools/configs_bench.py [--out profiles/r02_configs.json] [--quick]
 
-C2 / C3 / C5 evaluate the fitted maps (maps/); flare rows splat inside the query kernels.
-
-Times every kernel with CUDA events on the launching stream (3 warm-ups, median of
-repeats).  Inputs are generated by plt_inputs; for C3 (805 M queries) and the largest
-C5 sizes a resident 2^26-ray batch is re-used (tiled on the device) -- the timing is
-representative, the values repeat.  Not part of the driver's bench contract.
+C2, C3, C4_22, C4_59 and every C5 sweep size run through `bench.py --config ...` (the
+driver's contract: W warm-ups, K timed steps, CUDA events on the launching stream, NVML
+clocks) -- each JSON line carries the per-kernel times, the roofline of every kernel and of
+the dominant one.  C3 (805 M rays) and C5 (up to 2^30 rays) are generated on the device at
+full size by plt_gen_rays (no tiled inputs).  C1 (12,288 rays) is launch-bound; it is timed
+eagerly and as a CUDA-graph replay.  Not part of the driver's bench contract.
 """
 from __future__ import annotations
 
@@ -15,21 +16,24 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-import torch  # noqa: E402
 
-import paper_2605_04017_b200 as plt  # noqa: E402
-from plt_inputs import configs as C  # noqa: E402
-from plt_inputs import rays as R  # noqa: E402
+def bench_line(args: list) -> dict:
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--no-cpu-baseline"] + args
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1800)
+    if out.returncode != 0:
+        return {"error": out.stderr[-1500:], "args": args}
+    return json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
 
 
 def timed(fn, reps=5, warm=2):
+    import torch
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -44,30 +48,19 @@ def timed(fn, reps=5, warm=2):
     return statistics.median(ts)
 
 
-def tile_rays(d, n):
-    """Device rays of length n by tiling a resident batch (timing-only inputs)."""
-    m = d["ox"].numel()
-    if n <= m:
-        return {k: (v[:n] if k != "plane_z" else v) for k, v in d.items()}
-    rep = (n + m - 1) // m
-    return {k: (v.repeat(rep)[:n].contiguous() if k != "plane_z" else v) for k, v in d.items()}
-
-
-def valid_frac(h, n):
-    w = h["mask_bits"][: (n + 31) // 32].cpu().numpy().view(np.uint8)
-    return float(np.unpackbits(w).sum()) / n
-
-
 def c1():
+    import torch
+    import paper_2605_04017_b200 as plt
+    from plt_inputs import configs as C
     cfg = C.CONFIGS["C1"]
     lens = plt.Lens(C.lens_text("C1"), **cfg["opts"])
     d = plt.rays_to_device(C.c1_rays())
     n = d["ox"].numel()
     h = plt.alloc_hits(n)
+    flops = json.load(open(os.path.join(ROOT, "profiles", "trace_flops.json")))["configs"]["C1"]["4"]["flops_per_ray"]
     t = timed(lambda: plt.trace_rays(lens, lens.all_t_id(), d, h), reps=20)
     out = [{"config": "C1", "kernel": "trace_rays fp32", "rays": n, "ms": t * 1e3, "M_rays_s": n / t / 1e6,
-            "valid": valid_frac(h, n), "note": "launch-latency bound at 12,288 rays (per-call Python + launch)"}]
-    # the same call captured once in a CUDA graph and replayed 100x per timed sample
+            "TFLOPs": n * flops / t / 1e12, "note": "launch-latency bound at 12,288 rays (per-call Python + launch)"}]
     s = torch.cuda.Stream()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
@@ -77,104 +70,8 @@ def c1():
     reps = 100
     tg = timed(lambda: [g.replay() for _ in range(reps)], reps=5) / reps
     out.append({"config": "C1", "kernel": "trace_rays fp32, CUDA-graph replay", "rays": n, "ms": tg * 1e3,
-                "M_rays_s": n / tg / 1e6, "note": "trace + fp64 refine launches replayed from one graph"})
-    return out
-
-
-def c2(n=1 << 24):
-    cfg = C.CONFIGS["C2"]
-    lens = plt.Lens(C.lens_text("C2"), **cfg["opts"])
-    pid = lens.all_t_id()
-    m = plt.Map(C.fitted_map_blob("C2"), lens=lens)
-    d = plt.rays_to_device(R.gen_rays(cfg["law"], cfg["seed"], 0, n))
-    h = plt.alloc_hits(n)
-    out = []
-    for prec, name in ((plt.FP32, "trace_rays fp32"), (plt.FP64, "trace_rays fp64")):
-        t = timed(lambda: plt.trace_rays(lens, pid, d, h, precision=prec))
-        out.append({"config": "C2", "kernel": name, "rays": n, "ms": t * 1e3, "M_rays_s": n / t / 1e6,
-                    "valid": valid_frac(h, n)})
-    t = timed(lambda: plt.eval_map(m, d, h))
-    out.append({"config": "C2", "kernel": "eval_map", "rays": n, "ms": t * 1e3, "M_rays_s": n / t / 1e6,
-                "valid": valid_frac(h, n)})
-    return out
-
-
-def c3(total=192 * 128 * 32768, chunk=1 << 26):
-    cfg = C.CONFIGS["C3"]
-    lens = plt.Lens(C.lens_text("C3"), **cfg["opts"])
-    pid = lens.all_t_id()
-    m = plt.Map(C.fitted_map_blob("C3"), lens=lens)
-    base = plt.rays_to_device(R.gen_rays(cfg["law"], cfg["seed"], 0, 1 << 24))
-    d = tile_rays(base, chunk)
-    h = plt.alloc_hits(chunk)
-    n_chunks = total // chunk
-    out = []
-    t = timed(lambda: plt.trace_rays(lens, pid, d, h, direction=plt.BACKWARD), reps=3)
-    v = valid_frac(h, chunk)
-    out.append({"config": "C3", "kernel": "trace_rays fp32 backward", "rays": total, "ms": t * n_chunks * 1e3,
-                "M_rays_s": chunk / t / 1e6, "valid": v,
-                "note": f"{n_chunks} chunks of 2^26 (timed one chunk, resident tiled inputs)"})
-    t = timed(lambda: plt.eval_map(m, d, h), reps=3)
-    out.append({"config": "C3", "kernel": "eval_map backward", "rays": total, "ms": t * n_chunks * 1e3,
-                "M_rays_s": chunk / t / 1e6, "valid": valid_frac(h, chunk)})
-    return out
-
-
-def c4(name):
-    cfg = C.CONFIGS[name]
-    lens = plt.Lens(C.lens_text(name), **cfg["opts"])
-    ids, ij = lens.enumerate_ghosts(2)
-    ghosts = ids[1:]
-    npc = cfg["n_per_channel"]
-    film_d = cfg["film"]
-    chans = [plt.rays_to_device(C.flare_rays(name, c, 0, npc)) for c in range(3)]
-    h = plt.alloc_hits(npc)
-    film = torch.zeros(3 * film_d["height_px"] * film_d["width_px"], dtype=torch.int64, device="cuda")
-    chan_ids = [torch.full((npc,), c, dtype=torch.uint8, device="cuda") for c in range(3)]
-    maps = [plt.Map(C.map_blob(name, int(g), seed=int(g) % 100000)) for g in ghosts]
-    out = []
-    for prec, pname in ((plt.FP64, "fp64 (binding, A22)"), (plt.FP32, "fp32")):
-        def run():
-            film.zero_()
-            for g in ghosts:
-                for c in range(3):
-                    plt.trace_rays(lens, int(g), chans[c], h, precision=prec,
-                                   splat={"film_desc": film_d, "film": film, "channel": chan_ids[c],
-                                          "weight_scale": 1.0 / npc})
-        t = timed(run, reps=3, warm=1)
-        n = len(ghosts) * 3 * npc
-        out.append({"config": name, "kernel": f"flare: trace_rays {pname} + fused splat, {len(ghosts)} ghosts x 3 ch",
-                    "rays": n, "ms": t * 1e3, "M_rays_s": n / t / 1e6, "film_sum": int(film.sum().item())})
-
-    def run_map():
-        film.zero_()
-        for mi in maps:
-            for c in range(3):
-                plt.eval_map(mi, chans[c], h, splat={"film_desc": film_d, "film": film, "channel": chan_ids[c],
-                                                     "weight_scale": 1.0 / npc})
-    t = timed(run_map, reps=3, warm=1)
-    n = len(ghosts) * 3 * npc
-    out.append({"config": name, "kernel": f"flare: eval_map (seeded per-ghost maps) + fused splat, {len(ghosts)} ghosts",
-                "rays": n, "ms": t * 1e3, "M_rays_s": n / t / 1e6})
-    return out
-
-
-def c5(sizes):
-    cfg = C.CONFIGS["C5"]
-    lens = plt.Lens(C.lens_text("C5"), **cfg["opts"])
-    pid = lens.all_t_id()
-    m = plt.Map(C.fitted_map_blob("C2"), lens=lens)
-    base = plt.rays_to_device(R.gen_rays(cfg["law"], cfg["seed"], 0, 1 << 24))
-    out = []
-    for n in sizes:
-        d = tile_rays(base, n)
-        h = plt.alloc_hits(n)
-        tt = timed(lambda: plt.trace_rays(lens, pid, d, h), reps=3)
-        tm = timed(lambda: plt.eval_map(m, d, h), reps=3)
-        out.append({"config": "C5", "rays": n, "trace_ms": tt * 1e3, "trace_M_rays_s": n / tt / 1e6,
-                    "map_ms": tm * 1e3, "map_M_rays_s": n / tm / 1e6})
-        del d, h
-        torch.cuda.empty_cache()
+                "M_rays_s": n / tg / 1e6, "TFLOPs": n * flops / tg / 1e12,
+                "note": "trace + fp64 refine launches replayed from one graph; 12,288 rays cannot fill 148 SMs"})
     return out
 
 
@@ -182,21 +79,31 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--steps", type=int, default=10)
     a = ap.parse_args()
+    import torch
+    import paper_2605_04017_b200 as plt
     plt.load()
     res = {"gpu": torch.cuda.get_device_name(), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     res["C1"] = c1()
-    res["C2"] = c2()
-    res["C3"] = c3()
-    res["C4_22"] = c4("C4_22")
-    if not a.quick:
-        res["C4_59"] = c4("C4_59")
-    res["C5"] = c5([1 << k for k in ((20, 24) if a.quick else (20, 22, 24, 26, 28, 30))])
+    st = ["--steps", str(a.steps), "--warmup", "3"]
+    for name in ("C2", "C3", "C4_22", "C4_59"):
+        if a.quick and name == "C4_59":
+            continue
+        res[name] = bench_line(["--config", name] + (st if name != "C3" else ["--steps", "3", "--warmup", "3"]))
+        print(name, json.dumps({k: res[name].get(k) for k in ("value", "ms_per_step", "roofline")}), flush=True)
+    sizes = (20, 24) if a.quick else (20, 22, 24, 26, 28, 30)
+    res["C5"] = []
+    for k in sizes:
+        line = bench_line(["--config", "C5", "--rays", str(1 << k)] + st)
+        res["C5"].append(line)
+        print("C5 2^%d" % k, json.dumps({x: line.get(x) for x in ("value", "ms_per_step")}), flush=True)
     txt = json.dumps(res, indent=1)
-    print(txt)
     if a.out:
         with open(a.out, "w") as f:
             f.write(txt + "\n")
+    else:
+        print(txt)
 
 
 if __name__ == "__main__":
