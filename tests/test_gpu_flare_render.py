@@ -46,3 +46,58 @@ def test_flare_image_maps_vs_trace(gpu_lib, name):
     print(name, stats)
     assert abs(stats["energy"] - 1.0) <= 0.03
     assert stats["rel_l1_bin16"] <= 0.05 and stats["rel_l1_bin16"] < stats["mc_floor"]
+
+
+@pytest.mark.parametrize("name", ["C4_22", "C4_59"])
+def test_flare_image_fp64_vs_oracle_per_pixel(gpu_lib, name):
+    """NEXT-2 whole-image PARITY (Listing 1; Eq. 8): the GPU flare image
+    of every two-bounce ghost x RGB channel, 2^20 rays per channel, traced in float64
+    and splatted in-kernel (render_flare), against the oracle's trace + O11 film of the same
+    rays -- every pixel of every channel within SURVEY §8(c) film rule 2 (bin flips of rays
+    within the fp64 parity tolerance 4e-6 mm of a pixel edge, edge-band rays, the 2e-7 weight
+    tolerance), accumulated over all ghost x channel contributions."""
+    import numpy as np
+    import torch
+    import oracle
+    from gpu_helpers import assert_film_within_bound, film_pixel_bound, near_edge
+    from paper_2605_04017_b200.render import render_flare
+    plt = gpu_lib
+    cfg = C.CONFIGS[name]
+    fd, npc = cfg["film"], cfg["n_per_channel"]
+    lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+    ol = oracle.load_lens(C.lens_text(name), cfg["opts"])
+    ids, _ = lens.enumerate_ghosts(2)
+    ghosts = [int(g) for g in ids if int(g) != lens.all_t_id()]
+    rays_np = [C.flare_rays(name, c, 0, npc) for c in range(3)]
+    rays = [plt.rays_to_device(r) for r in rays_np]
+    film = torch.zeros(fd["channels"] * fd["height_px"] * fd["width_px"], dtype=torch.int64, device="cuda")
+    used = render_flare(lens, ghosts, rays, fd, film, precision=plt.FP64, weight_scale=1.0 / npc)
+    torch.cuda.synchronize()
+    assert all(u == "trace" for _, u in used) and len(used) == len(ghosts)
+    f_gpu = film.cpu().numpy().reshape(fd["channels"], fd["height_px"], fd["width_px"])
+    f_ora = np.zeros_like(f_gpu)
+    bound = np.zeros(f_gpu.shape, np.float64)
+    h = plt.alloc_hits(npc)
+    fd1 = dict(fd, channels=1)
+    threads = oracle.host_threads()
+    for g in ghosts:
+        for c in range(3):
+            o = oracle.trace(ol, g, 0, rays_np[c], threads=threads)
+            part, _ = oracle.splat(fd1, o["valid"], o["px"].astype(np.float32), o["py"].astype(np.float32),
+                                   o["dz"].astype(np.float32), o["I"].astype(np.float32), None, scale=1.0 / npc)
+            f_ora[c] += part[0]
+            amb = near_edge(o["margins"])
+            gpu_part = None
+            if amb.any():   # where the GPU put the edge-band rays (rule (b)): re-run that one path
+                plt.trace_rays(lens, g, rays[c], h, precision=plt.FP64)
+                torch.cuda.synchronize()
+                from gpu_helpers import unpack_mask
+                gpu_part = {"valid": unpack_mask(h["mask_bits"].cpu().numpy(), npc),
+                            **{k: h[kk].cpu().numpy().astype(np.float64)
+                               for k, kk in (("px", "px"), ("py", "py"), ("dz", "dz"), ("I", "throughput"))}}
+            else:
+                gpu_part = {"valid": np.zeros(npc, bool), "px": o["px"], "py": o["py"], "dz": o["dz"], "I": o["I"]}
+            bound[c] += film_pixel_bound(fd1, 1.0 / npc, o, gpu_part, amb, 4e-6, 2e-7)[0]
+    st = assert_film_within_bound(f_gpu, f_ora, bound, max_rel_bound=0.05)
+    print(name, "ghosts", len(ghosts), st)
+    assert st["diff_sum_rel"] <= 1e-3
