@@ -335,6 +335,14 @@ PLT_API plt_status plt_shade_plane(const plt_scene_plane* scene, double z_hits_m
  * IEEE double in that order (bit-identical to oracle.shade_plane with in_dz).
  * Errors: PLT_E_INVALID_ARG (also in_dz == NULL), PLT_E_CUDA.
  */
+/*
+ * The pupil-sampling factor A / dz^2 of plt_shade_plane_weighted for directions drawn through
+ * a uniform point of a disc of radius disc_r_mm at z = disc_z_mm, seen from a sensor at
+ * z = sensor_z_mm: *weight = pi disc_r^2 / (sensor_z - disc_z)^2 (the caller multiplies its
+ * own 1/spp into it).  Errors: PLT_E_INVALID_ARG (null, non-finite, r <= 0, disc on the sensor).
+ */
+PLT_API plt_status plt_pupil_weight(double sensor_z_mm, double disc_z_mm, double disc_r_mm, double* weight);
+
 PLT_API plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double z_hits_mm, const plt_hits* hits,
                                             int spp, int64_t pixels, float weight_scale, const float* in_dz,
                                             int64_t* film, int64_t n, void* cuda_stream);

@@ -30,7 +30,8 @@ EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "
             "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load", "plt_map_free", "plt_eval_map",
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
             "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_shade_cards",
-            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays", "plt_query_host")
+            "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays", "plt_query_host",
+            "plt_pupil_weight")
 
 
 class PltError(RuntimeError):
@@ -118,12 +119,13 @@ def load():
     L.plt_trace_kernel.argtypes = [p, u64, i, i, p]
     L.plt_gen_rays.argtypes = [p, u64, i64, p, i64, p]
     L.plt_query_host.argtypes = [p, u64, i, i, p, p, p, p, p, p, i64, i64, p]
+    L.plt_pupil_weight.argtypes = [d, d, d, p]
     L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
               "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted",
               "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays",
-              "plt_query_host"):
+              "plt_query_host", "plt_pupil_weight"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -489,6 +491,14 @@ def query_host(lens, path_id: int, m, host_rays: dict, film_desc: dict | None = 
                                  _host_ptr(film_host, npx, torch.int64) if film_host is not None else None,
                                  n, int(chunk), _stream(stream)))
     return film_host
+
+
+def pupil_weight(sensor_z_mm: float, disc_z_mm: float, disc_r_mm: float) -> float:
+    """plt_pupil_weight: pi r^2 / (sensor_z - disc_z)^2, the pupil-sampling factor of
+    plt_shade_plane_weighted."""
+    w = C.c_double()
+    _check(load().plt_pupil_weight(float(sensor_z_mm), float(disc_z_mm), float(disc_r_mm), C.byref(w)))
+    return w.value
 
 
 KERNEL_KINDS = {0: "jit", 1: "packed", 2: "scalar", 3: "fp64"}

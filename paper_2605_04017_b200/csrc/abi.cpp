@@ -368,6 +368,20 @@ plt_status plt_shade_plane_weighted(const plt_scene_plane* scene, double z_hits_
     return shade_impl(scene, z_hits_mm, hits, spp, pixels, weight_scale, in_dz, film, n, cuda_stream);
 }
 
+plt_status plt_pupil_weight(double sensor_z_mm, double disc_z_mm, double disc_r_mm, double* weight) {
+    PLT_GUARD_BEGIN
+    if (!weight) return set_err(PLT_E_INVALID_ARG, "weight is null");
+    const double dz = sensor_z_mm - disc_z_mm;
+    if (!std::isfinite(sensor_z_mm) || !std::isfinite(disc_z_mm) || !std::isfinite(disc_r_mm) || !(disc_r_mm > 0) ||
+        dz == 0.0)
+        return set_err(PLT_E_INVALID_ARG, "bad pupil disc");
+    // Eq. 9 estimator of pupil sampling (plt.h plt_shade_plane_weighted): solid-angle pdf
+    // dz^2 / (A cos^3 theta) with A = pi r^2; the cos^4 factor is applied per ray in-kernel
+    *weight = 3.14159265358979323846 * disc_r_mm * disc_r_mm / (dz * dz);
+    return PLT_OK;
+    PLT_GUARD_END
+}
+
 plt_status plt_propagate_rays(const plt_rays* in, const plt_rays* out, double z_target_mm, plt_dir dir, int64_t n,
                               void* cuda_stream) {
     PLT_RANGE("plt_propagate_rays");

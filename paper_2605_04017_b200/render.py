@@ -82,10 +82,8 @@ def render_dof(lens, rays: dict, scene: dict, film, spp: int, z_exit_mm: float, 
     if pupil_disc is not None:
         if rays.get("dz") is None:
             raise ValueError("pupil weighting needs the sensor rays' dz")
-        import math
-        z_disc, r_disc = float(pupil_disc[0]), float(pupil_disc[1])
-        dz = abs(float(rays["plane_z"]) - z_disc)
-        weight_scale = weight_scale * math.pi * r_disc ** 2 / dz ** 2
+        from . import pupil_weight
+        weight_scale = weight_scale * pupil_weight(rays["plane_z"], pupil_disc[0], pupil_disc[1])
         in_dz = rays["dz"]
     if "cards" in scene:   # several cards at different depths (plt_shade_cards)
         from . import shade_cards

@@ -339,3 +339,35 @@ def test_random_lenses_load_and_match_oracle_paraxials(plt, seed):
     oids, _ = oracle.enumerate_ghosts(O, 2)
     assert list(ids) == list(oids)
     assert L.trace_jit_cubin(L.all_t_id())[:4] == b"\x7fELF"
+
+
+def test_pupil_weight_and_new_entry_points_validate(plt):
+    """plt_pupil_weight is the closed form pi r^2 / dz^2 (host); plt_gen_rays / plt_query_host /
+    plt_trace_kernel validate their arguments before touching the device."""
+    import math
+    import torch
+    assert abs(plt.pupil_weight(52.0, 36.0, 9.8) - math.pi * 9.8 ** 2 / 16.0 ** 2) < 1e-15
+    assert abs(plt.pupil_weight(20.0, 36.0, 2.0) - math.pi * 4.0 / 256.0) < 1e-15
+    with pytest.raises(plt.PltError):
+        plt.pupil_weight(36.0, 36.0, 1.0)
+    with pytest.raises(plt.PltError):
+        plt.pupil_weight(50.0, 36.0, 0.0)
+    lib = plt.load()
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    rays = plt.Rays(*fake[:6], -5.0)
+    law = plt.RayLaw(0, 0, 0, 0, -5.0, 10.0, 0.0, 0.9, 0.0, 1.0, 0, 0, 0, 0, 400.0, 700.0)
+    bad = plt.RayLaw(7, 0, 0, 0, -5.0, 10.0, 0.0, 0.9, 0.0, 1.0, 0, 0, 0, 0, 400.0, 700.0)
+    grid = plt.RayLaw(3, 0, 16, 4, -5.0, 0, 0, 0, 0, 0, 24.0, 16.0, 36.0, 9.0, 400.0, 700.0)
+    if not torch.cuda.is_available():
+        assert lib.plt_gen_rays(C.byref(law), 1, 0, C.byref(rays), 10, None) == 6
+    assert lib.plt_gen_rays(C.byref(bad), 1, 0, C.byref(rays), 10, None) == 1
+    assert lib.plt_gen_rays(C.byref(grid), 1, 0, C.byref(rays), 10, None) == 1
+    assert lib.plt_gen_rays(C.byref(law), 1, -1, C.byref(rays), 10, None) == 1
+    assert lib.plt_gen_rays(C.byref(law), 1, 0, C.byref(rays), 0, None) == 0
+    L = plt.Lens(LENSES["dgauss50"])
+    assert lib.plt_query_host(L.handle, 1 << 10, 0, 0, None, C.byref(rays), None, None, None, None, 64, 33,
+                              None) == 1                                  # chunk not a multiple of 32
+    assert lib.plt_query_host(None, 0, 0, 0, None, C.byref(rays), None, None, None, None, 64, 32, None) == 1
+    k = C.c_int()
+    assert lib.plt_trace_kernel(L.handle, 1 << 10, 0, 1, C.byref(k)) == 0 and k.value == 3   # fp64
+    assert lib.plt_trace_kernel(L.handle, (1 << 10) | 1, 0, 0, C.byref(k)) == 1            # bad path id
