@@ -19,7 +19,7 @@
 //    would exceed the 2e-3 output tolerance (SURVEY [B3]);
 //  * biases are folded into the contraction (bf16 hi/mid/lo bias columns in B times a
 //    constant ones A tile shared by all groups in shared memory); epilogue per layer:
-//    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> one thread issues the
+//    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> warp 0 issues the
 //    next layer's MMAs (the 16 most logit-influential units of the classifier's first
 //    hidden layer -- ordered first at map load, map.cpp -- use the accurate
 //    1 - 2/(1 + 2^(2x log2 e)) instead of tanh.approx);
@@ -126,16 +126,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accum));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
     asm volatile(
@@ -175,13 +165,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
 __device__ __forceinline__ float bf16lo_f(uint32_t p) { return __uint_as_float(p << 16); }
 __device__ __forceinline__ float bf16hi_f(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
 
-__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
-                                        uint32_t accum) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
-        ::"r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
-}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                  ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
@@ -269,20 +252,36 @@ __device__ __forceinline__ Canon canonicalise(const MapParams& mp, float px, flo
     return k;
 }
 
-// Layer MMAs (A from TMEM, B = weights in shared memory).  Input layer: one K=16 step
-// (x hi/mid/lo + bias-ones).  Hidden / output layers: K = 64 of A from TMEM (32 hi, 32 lo)
-// plus one K = 16 step whose A is the shared constant ones tile in shared memory, against
-// B = [W | bias chunk] stored once as K = 48 (hi and lo reuse the same W columns).
-__device__ __forceinline__ void issue_input(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base) {
-    umma_ts(tmem_d, tmem_a, sdesc(b_base, 128, 256), idesc_bf16(32), 0u);
+// Layer MMAs (A from TMEM, B = weights in shared memory), issued with their commit by a
+// converged warp: elect.sync picks the issuing lane inside one asm block (the operands are
+// warp-uniform, so ptxas emits no per-MMA ELECT / R2UR.BROADCAST loop).  Input layer: one
+// K = 16 step (x hi/mid/lo + bias-ones).  Hidden / output layers: K = 64 of A from TMEM
+// (32 hi, 32 lo) plus one K = 16 step whose A is the shared constant ones tile in shared
+// memory, against B = [W | bias chunk] stored once as K = 48 (hi and lo reuse the same W).
+__device__ __forceinline__ void issue_input_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                 uint32_t bar) {
+    asm volatile(
+        "{\n.reg .pred p, f;\n"
+        "setp.ne.b32 f, 0, 0;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(bar) : "memory");
 }
-__device__ __forceinline__ void issue_hidden(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_base, uint32_t ones,
-                                             int n_out) {
-    const uint32_t id = idesc_bf16(n_out);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)   // h hi (ks 0, 1) and lo (ks 2, 3) against W k 0-15 / 16-31
-        umma_ts(tmem_d, tmem_a + 8 * ks, sdesc(b_base + (ks & 1) * 256, 128, 768), id, ks > 0 ? 1u : 0u);
-    umma(tmem_d, sdesc(ones, 128, 256), sdesc(b_base + 2 * 256, 128, 768), id, 1u);   // + bias
+__device__ __forceinline__ void issue_hidden_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b0, uint64_t b1,
+                                                  uint64_t onesd, uint64_t bb, uint32_t idesc, uint32_t bar) {
+    asm volatile(
+        "{\n.reg .pred p, f, t;\n.reg .b32 a1, a2, a3;\n"
+        "setp.ne.b32 f, 0, 0;\nsetp.eq.b32 t, 0, 0;\n"
+        "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %6, f;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %3, %6, t;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %6, t;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], %3, %6, t;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %6, t;\n"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n}\n"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(b0), "l"(b1), "l"(onesd), "l"(bb), "r"(idesc), "r"(bar) : "memory");
 }
 
 // Last hidden layer + fp32 output layer: h = tanh(D) from TMEM, y[o] = b[o] + sum_j W[o][j] h[j]
@@ -424,13 +423,19 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         tc_fence_before();
         group_bar(g);
         PLT_CLK(c1);
-        if (t == 0) {
+        if (q == 0) {   // warp 0 of the pipeline, converged: elect.sync inside the issue asm
             tc_fence_after();
             PLT_CLK(i0);
-            if (input) issue_input(tmem, tmem_a, w_base + b_off);
-            else issue_hidden(tmem, tmem_a, w_base + b_off, ones_base, n_out);
+            const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0), ta = __shfl_sync(0xffffffffu, tmem_a, 0);
+            const uint32_t bar = smem_u32(&S.bar_mma[g]);
+            if (input) {
+                issue_input_warp(tm, ta, sdesc(w_base + b_off, 128, 256), idesc_bf16(32), bar);
+            } else {
+                const uint32_t bb = w_base + b_off;
+                issue_hidden_warp(tm, ta, sdesc(bb, 128, 768), sdesc(bb + 256, 128, 768), sdesc(ones_base, 128, 256),
+                                  sdesc(bb + 512, 128, 768), idesc_bf16(n_out), bar);
+            }
             PLT_CLK(i1);
-            umma_commit(&S.bar_mma[g]);
 #ifdef PLT_MAP_PROFILE
             const long long i2 = clock64();
             pr_ifence += i0 - c1; pr_immas += i1 - i0; pr_icommit += i2 - i1;
