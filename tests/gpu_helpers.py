@@ -103,7 +103,8 @@ def film_pixel_bound(fd, scale, ora, gpu, ambiguous, tol_p, tol_wt):
     only come from (a) rays within tol_p of that pixel's edges (legitimate bin flips), (b)
     rays whose validity is ambiguous (edge band A23 / undecided logit A18) landing there on
     either side, and (c) the per-ray weight tolerance tol_wt of rays landing there
-    (|d(I |w_z|)|), plus 1 fixed-point unit of rounding per ray.
+    (|d(I |w_z|)|), plus 1 fixed-point unit where that tolerance straddles a rounding
+    boundary of the ray's fixed-point weight.
 
     ora / gpu: dicts with valid, px, py, dz, I and (optional) channel; positions in mm.
     tol_p, tol_wt: per-ray arrays (or scalars).  Returns the int64-unit bound (C, H, W)."""
@@ -125,8 +126,13 @@ def film_pixel_bound(fd, scale, ora, gpu, ambiguous, tol_p, tol_wt):
     amb = np.asarray(ambiguous, bool)
     near = (np.floor(fx - tp * pxs) != np.floor(fx + tp * pxs)) | (np.floor(fy - tp * pys) != np.floor(fy + tp * pys))
     cert = ov & ~amb & ~near
-    # (c) certain rays: same pixel on both sides, weights differ by <= tol_wt (I and w_z)
-    wc = (tol_wt * (np.abs(ora["I"]) + np.abs(ora["dz"]) + tol_wt)) * unit + 1.0
+    # (c) certain rays: same pixel on both sides, weights differ by <= delta = tol_wt (I and w_z);
+    # the two llrint() results then differ by at most delta, plus one unit only where
+    # [w - delta, w + delta] contains a half-integer (a rounding flip is possible there)
+    delta = (tol_wt * (np.abs(ora["I"]) + np.abs(ora["dz"]) + tol_wt)) * unit
+    w = np.abs(ora["I"]) * np.abs(ora["dz"]) * unit
+    flip = np.floor(w - delta + 0.5) != np.floor(w + delta + 0.5)
+    wc = delta + flip
     okp = cert & (fx >= 0) & (fx < Wp) & (fy >= 0) & (fy < Hp)
     np.add.at(bound, (ch[okp], np.floor(fy[okp]).astype(np.int64), np.floor(fx[okp]).astype(np.int64)), wc[okp])
     # (a) oracle-valid rays near a pixel edge: full weight in every pixel of their tolerance box
