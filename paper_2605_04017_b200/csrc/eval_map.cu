@@ -162,8 +162,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
     return d;
 }
-__device__ __forceinline__ float bf16lo_f(uint32_t p) { return __uint_as_float(p << 16); }
-__device__ __forceinline__ float bf16hi_f(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
 
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
@@ -179,10 +177,22 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // bias hi/mid/lo columns of B -- from the shared "ones" tile in shared memory.
 // hi + lo carries ~17 significant bits of h (the residual is exact in fp32 and rounded
 // once); the 3-term bias is exact for an fp32 bias.
+// The residuals x - hi come from the mixed-precision fma.rn.f32.bf16 (SASS FHFMA.BF16: one
+// instruction per element reads the bf16 half of the packed pair directly -- no unpacking
+// shift/mask), exact because |x - hi| <= 2^-9 |x| fits the fp32 mantissa of x.
+__device__ __forceinline__ void resid_pair(uint32_t hi, float x0, float x1, float& r0, float& r1) {
+    asm("{\n.reg .b16 h0, h1, m;\n"
+        "mov.b32 {h0, h1}, %2;\n"
+        "mov.b16 m, 0xBF80;\n"                       // bf16 -1.0
+        "fma.rn.f32.bf16 %0, h0, m, %3;\n"
+        "fma.rn.f32.bf16 %1, h1, m, %4;\n}\n"
+        : "=f"(r0), "=f"(r1) : "r"(hi), "f"(x0), "f"(x1));
+}
 __device__ __forceinline__ uint32_t split_pair(float x0, float x1, uint32_t& lo) {
     const uint32_t hi = pack_bf16(x0, x1);
-    const float2 r = __fadd2_rn(make_float2(x0, x1), make_float2(-bf16lo_f(hi), -bf16hi_f(hi)));   // exact
-    lo = pack_bf16(r.x, r.y);
+    float r0, r1;
+    resid_pair(hi, x0, x1, r0, r1);   // exact
+    lo = pack_bf16(r0, r1);
     return hi;
 }
 
@@ -202,9 +212,9 @@ __device__ __forceinline__ void store_input(uint32_t a_row, const float (&x)[4])
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
         const float x0 = x[2 * p], x1 = x[2 * p + 1];
-        uint32_t r;
-        v[p] = split_pair(x0, x1, r);
-        const float r0 = x0 - bf16lo_f(v[p]), r1 = x1 - bf16hi_f(v[p]);
+        v[p] = pack_bf16(x0, x1);
+        float r0, r1;
+        resid_pair(v[p], x0, x1, r0, r1);
         v[2 + p] = split_pair(r0, r1, v[4 + p]);
     }
     v[6] = 0x3F803F80u;   // bf16 (1.0, 1.0)

@@ -50,9 +50,14 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = statistics.median(ts)
+    hf = plt.alloc_hits(a.rays, flags=True)   # guard-band rays = the float64 re-trace list
+    plt.trace_rays(lens, pid, d, hf, direction=cfg["direction"], precision=prec)
+    torch.cuda.synchronize()
+    flagged = float(hf["flags"].float().mean())
     print(json.dumps({"tag": a.tag, "config": a.config, "path": pid, "rays": a.rays, "fp64": a.fp64, "ms": ms,
                       "M_rays_s": a.rays / ms / 1e3, "kernel": plt.trace_kernel(lens, pid, cfg["direction"], prec),
-                      "split_delta": os.environ.get("PLT_TRACE_SPLIT_DELTA", "0")}), flush=True)
+                      "split_delta": os.environ.get("PLT_TRACE_SPLIT_DELTA", "0"), "flagged_frac": flagged,
+                      "jit_defines": os.environ.get("PLT_JIT_DEFINES", "")}), flush=True)
 
 
 if __name__ == "__main__":
