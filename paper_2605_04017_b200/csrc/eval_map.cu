@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const int warp = tid >> 5;
     const int q = warp & 3;          // TMEM lane quarter
     const int lane = tid & 31;
+    const int issue_q = g & 3;       // the pipeline's MMA-issuing warp (see mma_layer)
     GroupSmem& Gs = S.g[g];
     constexpr uint32_t kTmemCols = 512;   // 32 accumulator + 32 A columns per pipeline, G <= 8
 
@@ -415,7 +416,10 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     uint32_t in_phase[2] = {0, 0};
 
     int64_t tile = group_id;
-    if (t == 0 && tile < P.n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
+    // the per-tile duties (tile claim, input TMA) go to lane 0 of warp (g + 2) mod 4: neither
+    // the MMA-issuing warp nor, for all pipelines, sub-partition 0
+    const int duty_t = 32 * ((g + 2) & 3);
+    if (t == duty_t && tile < P.n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
     mbar_wait(&S.bar_w, 0);
 
 #ifdef PLT_MAP_PROFILE
@@ -433,7 +437,11 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         tc_fence_before();
         group_bar(g);
         PLT_CLK(c1);
-        if (q == 0) {   // warp 0 of the pipeline, converged: elect.sync inside the issue asm
+        // one converged warp of the pipeline issues (elect.sync inside the issue asm): warp
+        // (g mod 4), so the 8 pipelines' issue work is spread over the 4 SM sub-partitions
+        // (warp q of every pipeline runs on sub-partition q; with warp 0 issuing for all of
+        // them, sub-partition 0 ran the slowest epilogues and every pipeline waited for it)
+        if (q == issue_q) {
             tc_fence_after();
             PLT_CLK(i0);
             const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0), ta = __shfl_sync(0xffffffffu, tmem_a, 0);
@@ -572,7 +580,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         const bool in_range = i < n;
         // claim the next tile and prefetch its inputs into the other stage (its previous
         // contents were consumed a tile ago); published to the group through next_tile[it & 1]
-        if (t == 0) {
+        if (t == duty_t) {
             const int64_t next = group_stride + (int64_t)atomicAdd(P.tile_ctr, 1);
             Gs.next_tile[it & 1] = next;
             if (next < P.n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);

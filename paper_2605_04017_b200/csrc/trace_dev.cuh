@@ -257,7 +257,11 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
         // relative to b^2 alone under-covers rays whose closest approach is near their
         // origin; the band used to cover every miss instead, re-tracing ~37 % of C3's rays)
         near = near | (alive & lt(abs2(disc), mk(kBandDisc) * (c + mk(st.R) * fma2(lz, mk(2.f), mk(st.R)))));
+#ifdef PLT_TRACE_EXPLICIT_KILLS
         alive = alive & le(mk(0.f), disc);
+#endif
+        // a miss (disc < 0) needs no test of its own: sqrt2_nc(disc) is NaN there, so t is NaN
+        // and the lane dies at t > eps below (comparisons with NaN are false)
         const f2 rt = sqrt2_nc(disc);
         // q = -(b + copysign(rt, b)) (b = -0 takes -rt: same root pair {q, c/q} = {-+rt, +-rt}).
         // q = 0 (b = disc = 0) needs no test: t is then 0, +-inf or NaN, and the lane dies at
@@ -325,7 +329,12 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
                                              : (st.is_R ? sel(tir, mk(1.f), Rf0) : Rf0);
 #endif
     if (!st.is_R) {
-        alive = alive & m2{!tir.x, !tir.y};   // TIR on a T step absorbs (A6)
+        // TIR on a T step absorbs (A6): cost = sqrt2_nc(kappa < 0) is NaN, so the new
+        // direction is NaN and the lane dies at the next step's direction test (or at the
+        // output plane's w_z > 0) -- no test here
+#ifdef PLT_TRACE_EXPLICIT_KILLS
+        alive = alive & m2{!tir.x, !tir.y};
+#endif
         const f2 g0 = fma2(eta, cosi, -cost);
         // g = w.n > 0 ? -g0 : g0 as a sign-bit flip (one LOP3 per lane); differs only at
         // w.n = +0 exactly (a ray exactly tangent to the surface: a measure-zero set)

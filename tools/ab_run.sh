@@ -1,22 +1,18 @@
-# Developer A/B on a GPU box (one call): trace variants.
+# Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/ab3
-TORCH_NVRTC=/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cuda_nvrtc/lib/libnvrtc.so.12
-for r in 1 2; do
-  for c in C2 C3; do
-    extra=""; [ $c = C3 ] && extra="--rays 67108864"
-    PLT_TRACE_QUEUE=0 python tools/trace_time_probe.py --config $c $extra --tag block >> $o.jsonl 2>&1
-    PLT_TRACE_QUEUE=1 python tools/trace_time_probe.py --config $c $extra --tag queue >> $o.jsonl 2>&1
-    PLT_TRACE_QUEUE=0 PLT_JIT_DEFINES="#define PLT_NEAR_UNGATED 1" python tools/trace_time_probe.py --config $c $extra --tag block-ungated >> $o.jsonl 2>&1
-    PLT_TRACE_QUEUE=0 PLT_NVRTC=$TORCH_NVRTC python tools/trace_time_probe.py --config $c $extra --tag block-nvrtc128 >> $o.jsonl 2>&1
-  done
+o=gpurun_out/ab8
+V=paper_2605_04017_b200
+for r in 1 2 3; do
+  python tools/map_time_probe.py --tag duty-claim-ahead >> $o.jsonl 2>&1
+  PLT_LIB=variants/libplt_duty.so python tools/map_time_probe.py --tag duty >> $o.jsonl 2>&1
 done
-PLT_TRACE_QUEUE=0 timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > $o.bench.json 2>&1
+PLT_LIB=$V/libplt_plt_map_profile.so python tools/map_time_probe.py --tag profile > $o.profile.log 2>&1
+python tools/logit_err_probe.py > $o.err.jsonl 2>&1
 python - <<'PY'
 import json
-for l in open("gpurun_out/ab3.jsonl"):
+for l in open("gpurun_out/ab8.jsonl"):
     if l.startswith("{"):
-        d = json.loads(l); print(d["tag"], d["config"], round(d["ms"], 4), d["kernel"], d["flagged_frac"])
+        d = json.loads(l); print(d["tag"], round(d["ms"], 4))
 PY
-tail -c 300 $o.bench.json
+grep "PROF blk0" $o.profile.log | tail -8; cat $o.err.jsonl
