@@ -120,6 +120,7 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
     L.cls_w[0] = place(32, 16); L.cls_w[1] = place(32, 48);
     L.reg_w[0] = place(32, 16);
     for (int l = 1; l < 5; ++l) L.reg_w[l] = place(32, 48);
+    L.reg_out = place(16, 48);
     L.out_off = (off + 15u) & ~15u;
     L.total_bytes = (L.out_off + 4u * kOutFloats + 15u) & ~15u;
     m->image.assign(L.total_bytes, 0);
@@ -179,17 +180,13 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
             const uint32_t fo = (uint32_t)dims[l + 1], fi = (uint32_t)dims[l];
             const std::vector<uint16_t>& W = Wl[head][l];
             const std::vector<float>& b = bl[head][l];
-            if (l + 1 == nl) {   // output layer: fp32 block
-                float* wo = outw + (head == 0 ? kOutClsW : kOutRegW);
-                float* bo = outw + (head == 0 ? kOutClsB : kOutRegB);
-                // classifier: W[0][k] as is; regressor: pair-interleaved Wp[p][k] = (W[2p][k], W[2p+1][k])
-                for (uint32_t o = 0; o < fo; ++o) {
-                    for (uint32_t k = 0; k < fi; ++k) {
-                        const size_t at = head == 0 ? o * fi + k : ((o / 2) * fi + k) * 2 + (o & 1);
-                        wo[at] = bf16_to_f(W[o * fi + k]);
-                    }
-                    bo[o] = b[o];
-                }
+            if (head == 1 && l + 1 == nl) {   // regressor output layer: N = 6 padded to 16, K = 48
+                pack_operand(m->image.data() + L.reg_out, W.data(), b.data(), (int)fo, (int)fi, 16, 48, false);
+                continue;
+            }
+            if (l + 1 == nl) {   // classifier output layer: fp32 block
+                for (uint32_t k = 0; k < fi; ++k) outw[kOutClsW + k] = bf16_to_f(W[k]);
+                outw[kOutClsB] = b[0];
                 continue;
             }
             const uint32_t woff = head == 0 ? L.cls_w[l] : L.reg_w[l];

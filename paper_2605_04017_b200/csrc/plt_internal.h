@@ -77,16 +77,17 @@ struct MapDims {
 // the bf16 hi/lo split of the fp32 bias, matched by constant-one columns in A.
 //   input layer : N=32, K=16 (W | W | b_hi b_lo 0..)        -> 1024 B
 //   hidden layer: N=32, K=48 (W[32] | b_hi b_lo 0.. | 0..)   -> 3072 B
-// The output layers (classifier 32->1, regressor 32->6) are evaluated in fp32 from the
-// last hidden activations (no MMA round): their weights (bf16 values widened) and biases
-// live in an fp32 block at `out_off`: cls W[32], cls b, pad to 4, reg W[6][32], reg b[6].
+// The classifier's output layer (32->1) is evaluated in fp32 from the last hidden
+// activations (no MMA round): its weights (bf16 values widened) and bias live in an fp32
+// block at `out_off`: W[32], b, pad to 4.  The regressor's (32->6) is an MMA operand.
 struct MapLayout {
     uint32_t cls_w[2];     // classifier input + hidden operands
     uint32_t reg_w[5];     // regressor input + 4 hidden operands
+    uint32_t reg_out;      // regressor output layer as an N = 16 operand (K = 48, like a hidden layer)
     uint32_t out_off;      // byte offset of the fp32 output-layer block (16-byte aligned)
     uint32_t total_bytes;  // multiple of 16
 };
-constexpr int kOutClsW = 0, kOutClsB = 32, kOutRegW = 36, kOutRegB = 36 + 192, kOutFloats = 36 + 192 + 8;
+constexpr int kOutClsW = 0, kOutClsB = 32, kOutFloats = 36;
 
 struct MapParams {
     float in_lo[4], in_scale[4];   // x_hat = clamp((x - lo) * scale - 1, -1, 1), scale = 2/(hi-lo)

@@ -1,18 +1,18 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/ab8
+o=gpurun_out/ab11
 V=paper_2605_04017_b200
 for r in 1 2 3; do
-  python tools/map_time_probe.py --tag duty-claim-ahead >> $o.jsonl 2>&1
-  PLT_LIB=variants/libplt_duty.so python tools/map_time_probe.py --tag duty >> $o.jsonl 2>&1
+  python tools/map_time_probe.py --tag base >> $o.jsonl 2>&1
+  PLT_LIB=$V/libplt_plt_map_reg_out_mma.so python tools/map_time_probe.py --tag reg-out-mma >> $o.jsonl 2>&1
 done
-PLT_LIB=$V/libplt_plt_map_profile.so python tools/map_time_probe.py --tag profile > $o.profile.log 2>&1
-python tools/logit_err_probe.py > $o.err.jsonl 2>&1
+PLT_LIB=$V/libplt_plt_map_reg_out_mma.so python tools/logit_err_probe.py --flare > $o.err.jsonl 2>&1
+PLT_LIB=$V/libplt_plt_map_reg_out_mma.so timeout 600 python -m pytest tests/test_gpu_fitted_maps.py tests/test_gpu_map_splat.py tests/test_gpu_fused_splat.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
 python - <<'PY'
 import json
-for l in open("gpurun_out/ab8.jsonl"):
+for l in open("gpurun_out/ab11.jsonl"):
     if l.startswith("{"):
-        d = json.loads(l); print(d["tag"], round(d["ms"], 4))
+        d = json.loads(l); print(d["tag"], d["map"], round(d["ms"], 4))
 PY
-grep "PROF blk0" $o.profile.log | tail -8; cat $o.err.jsonl
+cat $o.err.jsonl; tail -2 $o.tests.log

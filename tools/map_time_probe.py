@@ -25,12 +25,20 @@ def main():
     ap.add_argument("--rays", type=int, default=1 << 24)
     ap.add_argument("--tag", default=os.path.basename(os.environ.get("PLT_LIB", "libplt.so")))
     ap.add_argument("--map", default="C2")
+    ap.add_argument("--coherent", action="store_true",
+                    help="sort the rays by input position (rows, then columns): a pixel-ordered batch "
+                         "whose valid fraction varies coherently along the index range")
     a = ap.parse_args()
     cfg = C.CONFIGS[a.map]
     lens = plt.Lens(C.lens_text(a.map), **cfg["opts"])
     m = plt.Map(C.fitted_map_blob(a.map), lens=lens)
     n = a.rays
-    d = plt.rays_to_device(R.gen_rays(cfg["law"], cfg["seed"], 0, n), with_dz=False)
+    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
+    if a.coherent:
+        import numpy as np
+        order = np.lexsort((rays["ox"], np.round(rays["oy"], 1)))
+        rays = {k: (v[order] if hasattr(v, "shape") and getattr(v, "shape", ()) == (n,) else v) for k, v in rays.items()}
+    d = plt.rays_to_device(rays, with_dz=False)
     h = plt.alloc_hits(n)
     fd = {"width_px": 768, "height_px": 512, "channels": 1, "sensor_w_mm": 36.0, "sensor_h_mm": 24.0,
           "center_x_mm": 0.0, "center_y_mm": 0.0}
@@ -50,7 +58,7 @@ def main():
     w = h["mask_bits"].view(torch.int32)
     valid = float(sum(bin(x & 0xFFFFFFFF).count("1") for x in w[:4096].tolist())) / (4096 * 32)
     ms = statistics.median(ts)
-    print(json.dumps({"tag": a.tag, "map": a.map, "rays": n, "ms": ms, "M_rays_s": n / ms / 1e3,
+    print(json.dumps({"tag": a.tag, "map": a.map, "coherent": a.coherent, "rays": n, "ms": ms, "M_rays_s": n / ms / 1e3,
                       "valid_sample": valid, "min_ms": min(ts)}), flush=True)
 
 
