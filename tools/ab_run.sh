@@ -1,18 +1,22 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/ab11
+o=gpurun_out/ab15
 V=paper_2605_04017_b200
-for r in 1 2 3; do
-  python tools/map_time_probe.py --tag base >> $o.jsonl 2>&1
-  PLT_LIB=$V/libplt_plt_map_reg_out_mma.so python tools/map_time_probe.py --tag reg-out-mma >> $o.jsonl 2>&1
+for r in 1 2; do
+  for lib in $V/libplt_plt_fp64_full_newton.so $V/libplt.so; do
+    t=$(basename $lib .so)
+    PLT_LIB=$lib python tools/trace_time_probe.py --config C4_22 --path 65616 --fp64 --rays 1048576 --tag $t >> $o.jsonl 2>&1
+    PLT_LIB=$lib python tools/trace_time_probe.py --config C4_59 --path 16404 --fp64 --rays 1048576 --tag $t >> $o.jsonl 2>&1
+    PLT_LIB=$lib python tools/trace_time_probe.py --config C2 --fp64 --tag $t >> $o.jsonl 2>&1
+    PLT_LIB=$lib python tools/trace_time_probe.py --config C2 --tag $t >> $o.jsonl 2>&1
+  done
 done
-PLT_LIB=$V/libplt_plt_map_reg_out_mma.so python tools/logit_err_probe.py --flare > $o.err.jsonl 2>&1
-PLT_LIB=$V/libplt_plt_map_reg_out_mma.so timeout 600 python -m pytest tests/test_gpu_fitted_maps.py tests/test_gpu_map_splat.py tests/test_gpu_fused_splat.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
+timeout 900 python -m pytest tests/test_gpu_trace.py tests/test_gpu_flare_render.py tests/test_gpu_path_pruning.py tests/test_gpu_asphere.py tests/test_gpu_edge_cases.py tests/test_gpu_fuzz_lenses.py tests/test_gpu_unit_dirs.py tests/test_gpu_camera.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
 python - <<'PY'
 import json
-for l in open("gpurun_out/ab11.jsonl"):
+for l in open("gpurun_out/ab15.jsonl"):
     if l.startswith("{"):
-        d = json.loads(l); print(d["tag"], d["map"], round(d["ms"], 4))
+        d = json.loads(l); print(d["tag"], d["config"], d["path"], d["fp64"], round(d["ms"], 4))
 PY
-cat $o.err.jsonl; tail -2 $o.tests.log
+tail -n 3 $o.tests.log
