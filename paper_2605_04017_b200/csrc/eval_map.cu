@@ -21,8 +21,8 @@
 //    constant ones A tile shared by all groups in shared memory); epilogue per layer:
 //    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> warp 0 issues the
 //    next layer's MMAs (the 16 most logit-influential units of the classifier's first
-//    hidden layer -- ordered first at map load, map.cpp -- use the accurate
-//    1 - 2/(1 + 2^(2x log2 e)) instead of tanh.approx);
+//    hidden layer -- ordered first at map load, map.cpp -- use an accurate rational tanh
+//    instead of tanh.approx);
 //  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs;
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
 //    memory; the regressor only runs on full 128-row tiles of queued rays (plus one
@@ -161,6 +161,32 @@ __device__ __forceinline__ float tanh_accurate(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 2.8853900817779268f));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
     return fmaf(-2.f, r, 1.f);
+}
+// Accurate tanh for a PAIR of units on the FMA pipe with one MUFU reciprocal each:
+// tanh(x) ~= x P(x^2) / Q(x^2) on |x| <= 8.5 (clamped beyond: tanh(8.5) = 1 - 8e-8), P and
+// Q of degree 4 fitted by tools/fit_tanh_rational.py (float64 fit error 1.1e-8; float32
+// evaluation |error| <= 3.3e-7, as accurate as ex2 + rcp).  Packed FFMA2 Horner steps serve
+// both units; per pair 2 MUFU instead of 4 -- MUFU is eval_map's bound.
+__device__ __forceinline__ void tanh_rational2(float& x0, float& x1) {
+    constexpr float kXMax = 8.5f;
+    const float2 x = make_float2(fminf(fmaxf(x0, -kXMax), kXMax), fminf(fmaxf(x1, -kXMax), kXMax));
+    const float2 s = __fmul2_rn(x, x);
+    auto c2 = [](float c) { return make_float2(c, c); };
+    float2 P = c2(0x1.e48b04p-27f);
+    P = __ffma2_rn(P, s, c2(0x1.6264eap-16f));
+    P = __ffma2_rn(P, s, c2(0x1.ce26d2p-9f));
+    P = __ffma2_rn(P, s, c2(0x1.128fa6p-3f));
+    P = __ffma2_rn(P, s, c2(0x1.fffffep-1f));
+    float2 Q = c2(0x1.b18288p-21f);
+    Q = __ffma2_rn(Q, s, c2(0x1.5dcaf6p-12f));
+    Q = __ffma2_rn(Q, s, c2(0x1.a9d89ap-6f));
+    Q = __ffma2_rn(Q, s, c2(0x1.de9d1ap-2f));
+    Q = __ffma2_rn(Q, s, c2(1.f));
+    float r0, r1;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(Q.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(Q.y));
+    const float2 t = __fmul2_rn(__fmul2_rn(x, P), make_float2(r0, r1));
+    x0 = t.x; x1 = t.y;
 }
 #ifndef PLT_MAP_CLS_ACCURATE_UNITS
 #define PLT_MAP_CLS_ACCURATE_UNITS 16   // most logit-influential classifier h1 units with the accurate tanh
@@ -463,8 +489,11 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             // the first PLT_MAP_CLS_ACCURATE_UNITS take the accurate tanh
             if (accurate && 16 * half < PLT_MAP_CLS_ACCURATE_UNITS) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    v[j] = 16 * half + j < PLT_MAP_CLS_ACCURATE_UNITS ? tanh_accurate(v[j]) : tanh_approx(v[j]);
+                for (int j = 0; j < 16; j += 2) {
+                    if (16 * half + j + 1 < PLT_MAP_CLS_ACCURATE_UNITS) tanh_rational2(v[j], v[j + 1]);
+                    else if (16 * half + j < PLT_MAP_CLS_ACCURATE_UNITS) { v[j] = tanh_accurate(v[j]); v[j + 1] = tanh_approx(v[j + 1]); }
+                    else { v[j] = tanh_approx(v[j]); v[j + 1] = tanh_approx(v[j + 1]); }
+                }
             } else {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);

@@ -1,17 +1,18 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/ab16
-for r in 1 2; do
-  python tools/trace_time_probe.py --config C2 --tag idx32 >> $o.jsonl 2>&1
-  python tools/trace_time_probe.py --config C3 --rays 67108864 --tag idx32 >> $o.jsonl 2>&1
-  PLT_TRACE_JIT=0 python tools/trace_time_probe.py --config C2 --tag idx32-generic >> $o.jsonl 2>&1
+o=gpurun_out/ab17
+V=paper_2605_04017_b200
+for r in 1 2 3; do
+  python tools/map_time_probe.py --tag rational >> $o.jsonl 2>&1
+  PLT_LIB=$V/libplt_plt_map_acc_ex2.so python tools/map_time_probe.py --tag ex2 >> $o.jsonl 2>&1
 done
-timeout 900 python -m pytest tests/test_gpu_trace.py tests/test_gpu_trace_jit.py tests/test_gpu_fused_splat.py tests/test_gpu_edge_cases.py tests/test_gpu_unit_dirs.py tests/test_gpu_full_range.py tests/test_gpu_graph.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
+python tools/logit_err_probe.py --flare > $o.err.jsonl 2>&1
+PLT_LIB=$V/libplt_plt_map_acc_ex2.so python tools/logit_err_probe.py --flare > $o.err_ex2.jsonl 2>&1
 python - <<'PY'
 import json
-for l in open("gpurun_out/ab16.jsonl"):
+for l in open("gpurun_out/ab17.jsonl"):
     if l.startswith("{"):
-        d = json.loads(l); print(d["tag"], d["config"], d["path"], round(d["ms"], 4), d["flagged_frac"])
+        d = json.loads(l); print(d["tag"], d["map"], round(d["ms"], 4))
 PY
-tail -n 3 $o.tests.log
+echo rational; cat $o.err.jsonl; echo ex2; cat $o.err_ex2.jsonl
