@@ -1,18 +1,18 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/ab17
-V=paper_2605_04017_b200
+o=gpurun_out/ab18
 for r in 1 2 3; do
-  python tools/map_time_probe.py --tag rational >> $o.jsonl 2>&1
-  PLT_LIB=$V/libplt_plt_map_acc_ex2.so python tools/map_time_probe.py --tag ex2 >> $o.jsonl 2>&1
+  python tools/map_time_probe.py --tag preissue >> $o.jsonl 2>&1
+  PLT_LIB=variants/libplt_rational.so python tools/map_time_probe.py --tag base >> $o.jsonl 2>&1
 done
-python tools/logit_err_probe.py --flare > $o.err.jsonl 2>&1
-PLT_LIB=$V/libplt_plt_map_acc_ex2.so python tools/logit_err_probe.py --flare > $o.err_ex2.jsonl 2>&1
+python tools/logit_err_probe.py > $o.err.jsonl 2>&1
+timeout 600 python -m pytest tests/test_gpu_fitted_maps.py tests/test_gpu_map_splat.py tests/test_gpu_fused_splat.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
 python - <<'PY'
 import json
-for l in open("gpurun_out/ab17.jsonl"):
+for l in open("gpurun_out/ab18.jsonl"):
     if l.startswith("{"):
         d = json.loads(l); print(d["tag"], d["map"], round(d["ms"], 4))
+    else: print(l[:300])
 PY
-echo rational; cat $o.err.jsonl; echo ex2; cat $o.err_ex2.jsonl
+cat $o.err.jsonl; tail -n 2 $o.tests.log
