@@ -125,6 +125,28 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
+def bind_numa_local(dev: int) -> str:
+    """Pin this process to the CPU cores NVML reports as closest to GPU `dev` (its NUMA
+    node), so the pinned host buffers of the e2e leg are first-touched in that node's memory
+    and each rank's host->device copies of a multi-GPU run use the local socket's memory
+    bandwidth.  Best effort: returns a note, never raises."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(dev)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if not cpus:
+            return "cpu affinity: none reported"
+        os.sched_setaffinity(0, cpus)
+        return f"bound to the {len(cpus)} cores local to the GPU"
+    except Exception as ex:   # no NVML / no affinity support: keep the default placement
+        return f"cpu affinity unchanged ({type(ex).__name__})"
+
+
 def dist_setup(args):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -138,6 +160,8 @@ def dist_setup(args):
         if share:
             local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
+        if not share and ws > 1:   # N = 1 keeps every core (the oracle baseline uses them)
+            args.numa = bind_numa_local(local)
     if ws > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -579,7 +603,8 @@ def run_plt(args, ws, rank, local):
         "metric": METRIC, "value": rays_all / step_s / 1e6, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": dict(cfg_line, name=name, **extra_cfg),
+        "config": dict(cfg_line, name=name, **extra_cfg,
+                       **({"host_affinity": args.numa} if getattr(args, "numa", None) else {})),
         "roofline": roof,
         "kernels": kernels,
         "e2e": ({"value": rays_all / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
