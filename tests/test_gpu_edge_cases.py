@@ -61,3 +61,33 @@ def test_rays_missing_the_lens_and_axial_rays(gpu_lib):
         compare_trace(g, o, excluded_max=32)           # the 32 grazing rays have |w_z| = 0
         assert not g["valid"][:32].any() and g["valid"][32:64].all() and not g["valid"][64:].any()
         assert np.abs(g["px"][32:64]).max() == 0.0 and np.abs(g["py"][32:64]).max() == 0.0
+
+
+def test_total_internal_reflection_and_sphere_misses(gpu_lib):
+    """Eq. 6-7 branches the kernels take without a comparison of their own (DESIGN.md "Misses
+    and TIR die through NaN"): a ray missing a spherical cap (disc < 0) and a ray totally
+    internally reflected on a transmission step (A6: absorbed) are invalid with zero outputs,
+    exactly as the oracle's explicit tests (pinned in test_oracle_trace) decide, in fp32 and
+    fp64 (the generic packed and scalar fp32 kernels: the same test under PLT_TRACE_JIT=0 /
+    PLT_TRACE_X1=1).  Lens: n = 2 front cap (R = 10 mm) + planar rear; parallel rays at
+    heights 0 ... 12 mm: below 7.14 mm they transmit, higher ones are bent past the 30 deg
+    critical angle at the rear face, above 10 mm they miss the cap."""
+    plt = gpu_lib
+    text = "name tir\n10 3.0 n:2.0 20\n0 0 air 40\n"
+    opts = {"sensor_z_mm": 20.0}
+    gl = plt.Lens(text, **opts)
+    ol = oracle.load_lens(text, opts)
+    n = 4096
+    rng = np.random.default_rng(5)
+    h = np.linspace(0.0, 12.0, n)
+    phi = rng.uniform(0, 2 * np.pi, n)
+    rays = {"ox": (h * np.cos(phi)).astype(np.float32), "oy": (h * np.sin(phi)).astype(np.float32),
+            "dx": np.zeros(n, np.float32), "dy": np.zeros(n, np.float32), "dz": np.ones(n, np.float32),
+            "lambda_nm": rng.uniform(400, 700, n).astype(np.float32), "plane_z": -5.0}
+    pid = gl.all_t_id()
+    o = oracle.trace(ol, pid, 0, rays)
+    assert o["valid"][h < 7.0].all()                     # transmitted
+    assert not o["valid"][(h > 7.3) & (h < 9.99)].any()   # TIR at the rear face
+    assert not o["valid"][h > 10.01].any()               # misses the cap
+    for prec in (plt.FP32, plt.FP64):
+        compare_trace(gpu_trace(plt, gl, pid, rays, precision=prec), o)
