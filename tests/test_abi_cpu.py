@@ -371,3 +371,19 @@ def test_pupil_weight_and_new_entry_points_validate(plt):
     k = C.c_int()
     assert lib.plt_trace_kernel(L.handle, 1 << 10, 0, 1, C.byref(k)) == 0 and k.value == 3   # fp64
     assert lib.plt_trace_kernel(L.handle, (1 << 10) | 1, 0, 0, C.byref(k)) == 1            # bad path id
+
+
+def test_jit_uses_the_toolkit_nvrtc_even_with_torch_loaded(plt):
+    """The run-time specialised trace is compiled by the CUDA toolkit's NVRTC (the release
+    that builds the ahead-of-time kernels), not by whichever libnvrtc.so.12 the process has
+    already loaded (torch bundles an older one, whose code for the same source measured 9 %
+    more instructions).  The cubin records its compiler release."""
+    import re
+    import subprocess
+    import torch  # noqa: F401  (loads torch's libraries first, as bench.py and the tests do)
+    nvcc = subprocess.run(["/usr/local/cuda/bin/nvcc", "--version"], capture_output=True, text=True).stdout
+    release = re.search(r"release (\d+\.\d+)", nvcc).group(1)
+    L = plt.Lens(LENSES["dgauss50"])
+    cubin = L.trace_jit_cubin(L.all_t_id())
+    m = re.search(rb"Cuda compilation tools, release (\d+\.\d+)", cubin)
+    assert m and m.group(1).decode() == release, (m.group(0) if m else None, release)
