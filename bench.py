@@ -533,21 +533,47 @@ def run_plt(args, ws, rank, local):
         h = plt.alloc_hits(npc, dev)
         film = torch.zeros(fd["channels"] * fd["height_px"] * fd["width_px"], dtype=torch.int64, device=dev)
         ev = Events(["trace_rays", "eval_map", "film_allreduce"], args.steps, stream)
+        # the image's (ghost, channel) launches are independent (int64 atomics into one film:
+        # order-free, bit-identical), so they go round-robin over a few side streams, each with
+        # its own hit buffer: one launch's tail overlaps the next one's start
+        n_side = max(1, args.flare_streams)
+        sides = [torch.cuda.Stream(device=dev) for _ in range(n_side)] if n_side > 1 else [stream]
+        hs = [h] + [plt.alloc_hits(npc, dev) for _ in range(len(sides) - 1)]
+        fork_ev = [torch.cuda.Event() for _ in range(2)]
+        join_ev = [[torch.cuda.Event() for _ in sides] for _ in range(2)]
 
         def view(d, i0, cnt):
             return {k: (v[i0:i0 + cnt] if k != "plane_z" and v is not None else v) for k, v in d.items()}
 
+        def fan_out(phase, launch):
+            if len(sides) > 1:
+                fork_ev[phase].record(stream)
+                for sd in sides:
+                    sd.wait_event(fork_ev[phase])
+            for j, seg in enumerate(segs):
+                launch(seg, sides[j % len(sides)], hs[j % len(sides)])
+            if len(sides) > 1:
+                for sd, e in zip(sides, join_ev[phase]):
+                    e.record(sd)
+                    stream.wait_event(e)
+
         def step(k):
             film.zero_()
             ev.mark(k, 0)
-            for g, c, i0, cnt in segs:
+
+            def tr(seg, sd, hh):
+                g, c, i0, cnt = seg
                 spl = {"film_desc": fd, "film": film, "channel": chan_ids[c][i0:i0 + cnt], "weight_scale": 1.0 / npc}
-                plt.trace_rays(lens, g, view(chans[c], i0, cnt), h, precision=plt.FP64, n=cnt, stream=stream,
+                plt.trace_rays(lens, g, view(chans[c], i0, cnt), hh, precision=plt.FP64, n=cnt, stream=sd,
                                splat=spl)
-            ev.mark(k, 1)
-            for g, c, i0, cnt in segs:
+
+            def mp(seg, sd, hh):
+                g, c, i0, cnt = seg
                 spl = {"film_desc": fd, "film": film, "channel": chan_ids[c][i0:i0 + cnt], "weight_scale": 1.0 / npc}
-                plt.eval_map(maps[g], view(chans[c], i0, cnt), h, n=cnt, stream=stream, splat=spl)
+                plt.eval_map(maps[g], view(chans[c], i0, cnt), hh, n=cnt, stream=sd, splat=spl)
+            fan_out(0, tr)
+            ev.mark(k, 1)
+            fan_out(1, mp)
             ev.mark(k, 2)
             if dist is not None:
                 dist.all_reduce(film)
@@ -683,6 +709,8 @@ def main():
                     help="BASELINE.json workload: C2 (default, the N=1 headline), C3, C4_22, C4_59, C5")
     ap.add_argument("--rays", type=int, default=0, help="rays per GPU per step (C2: 2^24, C5: 2^30 by default)")
     ap.add_argument("--dump-film", default=None, help="(C4) save rank 0's final film (.npy) -- for tests")
+    ap.add_argument("--flare-streams", type=int, default=2,
+                    help="(C4) side streams the image's independent (ghost, channel) launches go round-robin over")
     ap.add_argument("--ref-rays", type=int, default=1 << 15, help="rays per oracle step (--impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="rays per H2D chunk of the e2e leg")
