@@ -1,15 +1,22 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
-mkdir -p gpurun_out
-o=gpurun_out/ab23
-for c in C4_22 C4_59; do
-  for fs in 1 2 4 8; do
-    timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --flare-streams $fs --dump-film gpurun_out/film_${c}_$fs.npy 2>/dev/null | tail -1 | python -c "
-import json,sys
-d=json.loads(sys.stdin.read()); print('$c', $fs, round(d['ms_per_step'],3), {k:round(v['ms'],3) for k,v in d['kernels'].items()})"
+o=gpurun_out/ab25
+for r in 1 2; do
+  for c in C2 C3; do
+    extra=""; [ $c = C3 ] && extra="--rays 67108864"
+    timeout 120 python tools/trace_time_probe.py --config $c $extra --tag early >> $o.jsonl 2>&1
+    PLT_TRACE_NO_EARLY=1 timeout 120 python tools/trace_time_probe.py --config $c $extra --tag none >> $o.jsonl 2>&1
+    PLT_TRACE_JIT=0 timeout 120 python tools/trace_time_probe.py --config $c $extra --tag early-generic >> $o.jsonl 2>&1
+    PLT_TRACE_JIT=0 PLT_TRACE_NO_EARLY=1 timeout 120 python tools/trace_time_probe.py --config $c $extra --tag none-generic >> $o.jsonl 2>&1
   done
-  python -c "
-import numpy as np
-a=[np.load('gpurun_out/film_${c}_%d.npy'%f) for f in (1,2,4,8)]
-print('films identical:', all(np.array_equal(a[0], x) for x in a[1:]))"
 done
+timeout 600 python -m pytest tests/test_gpu_trace.py tests/test_gpu_trace_jit.py tests/test_gpu_fused_splat.py tests/test_gpu_edge_cases.py tests/test_gpu_full_range.py tests/test_gpu_camera.py tests/test_gpu_determinism.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
+PLT_TRACE_JIT=0 timeout 600 python -m pytest tests/test_gpu_trace.py tests/test_gpu_edge_cases.py tests/test_gpu_fuzz_lenses.py -q > $o.tests_g.log 2>&1; echo "exit $?" >> $o.tests_g.log
+python - <<'PY'
+import json
+for l in open("gpurun_out/ab25.jsonl"):
+    if l.startswith("{"):
+        d = json.loads(l); print(d["tag"], d["config"], round(d["ms"], 4), d["flagged_frac"])
+    else: print(l[:200])
+PY
+tail -n 2 $o.tests.log $o.tests_g.log
