@@ -16,7 +16,9 @@ import pytest
 from plt_inputs import configs as C
 from plt_inputs import rays as R
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("PLT_TRACE_JIT") == "0" or bool(os.environ.get("PLT_TRACE_X1")),
+                                 reason="the process runs with the JIT kernel switched off (developer knob)")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
