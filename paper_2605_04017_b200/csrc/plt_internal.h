@@ -106,6 +106,7 @@ struct SplatCtx {
     double W, H, cx, cy;
     int width, height, channels;
     float scale;
+    double wscale;                        // (double)scale * 2^32, exact (a power-of-two factor)
     float cxf, cyf, hwf, hhf, sxf, syf;   // fp32 fast-path constants
     float guard;                          // fp32 pixel-coordinate error bound (px), see make_splat_ctx
 };
@@ -117,6 +118,7 @@ inline SplatCtx make_splat_ctx(const plt_film_desc& fd, int64_t* film, const uin
     c.W = fd.sensor_w_mm; c.H = fd.sensor_h_mm; c.cx = fd.center_x_mm; c.cy = fd.center_y_mm;
     c.width = fd.width_px; c.height = fd.height_px; c.channels = fd.channels;
     c.scale = scale;
+    c.wscale = (double)scale * 4294967296.0;
     c.cxf = (float)fd.center_x_mm; c.cyf = (float)fd.center_y_mm;
     c.hwf = (float)(0.5 * c.W); c.hhf = (float)(0.5 * c.H);
     c.sxf = (float)(fd.width_px / c.W); c.syf = (float)(fd.height_px / c.H);

@@ -27,15 +27,27 @@ __device__ __forceinline__ int splat_key(const SplatCtx& c, float px, float py, 
     // floor equals the floor of the exact double expression of O11; only hits near a pixel
     // edge evaluate the double expression (bit-exact film for any film size).
     const float fxs = (px - c.cxf + c.hwf) * c.sxf, fys = (c.hhf - (py - c.cyf)) * c.syf;
-    double fxf = floorf(fxs), fyf = floorf(fys);
+    int ix, iy;
+    bool in;
     if (fabsf(fxs - rintf(fxs)) < c.guard || fabsf(fys - rintf(fys)) < c.guard) {
         const double fx = __dmul_rn(__ddiv_rn(__dadd_rn(__dsub_rn((double)px, c.cx), c.W * 0.5), c.W), (double)c.width);
         const double fy = __dmul_rn(__ddiv_rn(__dsub_rn(c.H * 0.5, __dsub_rn((double)py, c.cy)), c.H), (double)c.height);
-        fxf = floor(fx); fyf = floor(fy);
+        const double fxf = floor(fx), fyf = floor(fy);
+        in = fxf >= 0.0 && fxf < (double)c.width && fyf >= 0.0 && fyf < (double)c.height;
+        ix = in ? (int)fxf : 0;
+        iy = in ? (int)fyf : 0;
+    } else {
+        // no pixel edge (integer) within the error bound: signs and floors of the fp32 estimate
+        // are those of O11's double expression; NaN fails the >= 0 tests, far hits saturate
+        ix = __float2int_rd(fxs);
+        iy = __float2int_rd(fys);
+        in = fxs >= 0.f && fys >= 0.f && ix < c.width && iy < c.height;
     }
-    if (fxf >= 0.0 && fxf < (double)c.width && fyf >= 0.0 && fyf < (double)c.height && ch < c.channels) {
-        w = __double2ll_rn(__dmul_rn(__dmul_rn(__dmul_rn((double)I, fabs((double)dz)), (double)c.scale), 4294967296.0));
-        return (ch * c.height + (int)fyf) * c.width + (int)fxf;
+    if (in && ch < c.channels) {
+        // (I |w_z| scale) 2^32 with ONE rounding after I |w_z| (exact in double) as in O11: the
+        // factor 2^32 is exact, so multiplying by scale 2^32 rounds identically
+        w = __double2ll_rn(__dmul_rn(__dmul_rn((double)I, fabs((double)dz)), c.wscale));
+        return (ch * c.height + iy) * c.width + ix;
     }
     drop = true;
     return -1;
