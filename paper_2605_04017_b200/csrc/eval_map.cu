@@ -58,7 +58,7 @@ struct GroupSmem {
     float qc[kQueue], qs[kQueue];            // rotation (cos, sin) to undo
     int qi[kQueue];                          // ray index | reflection flag << 31
     int wcount[4];                           // per-warp valid counts (prefix)
-    int64_t next_tile[2];                    // dynamic scheduler: the group's next tile (by parity)
+    int next_tile[2];                        // dynamic scheduler: the group's next tile (by parity)
     long long wsum[kTile];                   // fused splat: per-warp aggregation slots
 };
 
@@ -403,14 +403,16 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         tma_bulk_g2s(S.w, P.wimg, P.lay.total_bytes, &S.bar_w);
     }
 
-    const int64_t n = P.n;
-    const int64_t group_id = (int64_t)blockIdx.x * G + g;
-    const int64_t group_stride = (int64_t)gridDim.x * G;
-    auto tile_full_tma = [&](int64_t tile) { return P.tma_ok && (tile + 1) * kTile <= n; };
-    auto issue_stage = [&](int64_t tile, int st) {   // one thread of the group
+    // ray indices < 2^31 per call (checked at the ABI): 32-bit index arithmetic
+    const int n = (int)P.n;
+    const int n_tiles = (int)P.n_tiles;
+    const int group_id = (int)blockIdx.x * G + g;
+    const int group_stride = (int)gridDim.x * G;
+    auto tile_full_tma = [&](int tile) { return P.tma_ok && tile < n / kTile; };
+    auto issue_stage = [&](int tile, int st) {   // one thread of the group
         fence_proxy_async();
         mbar_expect_tx(&S.bar_in[g][st], kStageBytes);
-        const int64_t o = tile * kTile;
+        const int o = tile * kTile;
         tma_bulk_g2s(Gs.stage[st][0], P.in.ox + o, kTile * 4, &S.bar_in[g][st]);
         tma_bulk_g2s(Gs.stage[st][1], P.in.oy + o, kTile * 4, &S.bar_in[g][st]);
         tma_bulk_g2s(Gs.stage[st][2], P.in.dx + o, kTile * 4, &S.bar_in[g][st]);
@@ -423,11 +425,11 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     uint32_t mma_phase = 0;
     uint32_t in_phase[2] = {0, 0};
 
-    int64_t tile = group_id;
+    int tile = group_id;
     // the per-tile duties (tile claim, input TMA) go to lane 0 of warp (g + 2) mod 4: neither
     // the MMA-issuing warp nor, for all pipelines, sub-partition 0
     const int duty_t = 32 * ((g + 2) & 3);
-    if (t == duty_t && tile < P.n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
+    if (t == duty_t && tile < n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
     mbar_wait(&S.bar_w, 0);
 
 #ifdef PLT_MAP_PROFILE
@@ -594,17 +596,17 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     // atomicAdd per tile hands the next one to whichever pipeline is free, so pipelines
     // whose tiles held more valid rays (more regressor work) take fewer tiles and the
     // SMs finish together
-    for (int it = 0; tile < P.n_tiles; ++it) {
+    for (int it = 0; tile < n_tiles; ++it) {
         const int st = it & 1;
-        const int64_t base = tile * kTile;
-        const int64_t i = base + t;
+        const int base = tile * kTile;
+        const int i = base + t;
         const bool in_range = i < n;
         // claim the next tile and prefetch its inputs into the other stage (its previous
         // contents were consumed a tile ago); published to the group through next_tile[it & 1]
         if (t == duty_t) {
-            const int64_t next = group_stride + (int64_t)atomicAdd(P.tile_ctr, 1);
+            const int next = group_stride + atomicAdd(P.tile_ctr, 1);
             Gs.next_tile[it & 1] = next;
-            if (next < P.n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
+            if (next < n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
         }
         PLT_CLK(o0);
         float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
@@ -658,7 +660,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             Gs.qi[slot] = (int)i | (k.flip ? (int)0x80000000u : 0);
         }
         qcount += total;
-        const int64_t next_tile = Gs.next_tile[it & 1];   // written before the group barrier above
+        const int next_tile = Gs.next_tile[it & 1];   // written before the group barrier above
         PLT_CLK(o5);
         if (qcount >= kTile) run_regressor(kTile);
 #ifdef PLT_MAP_PROFILE
