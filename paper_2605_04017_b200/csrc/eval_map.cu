@@ -93,16 +93,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t phase) {
         "}\n" : "=r"(ok) : "r"(smem_u32(b)), "r"(phase) : "memory");
     return ok != 0;
 }
-// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.  The
-// clock is only consulted every 64 polls.  (Measured alternatives: try_wait with
-// a suspend-time hint, a clock-free poll loop, one polling warp per pipeline -- none faster.)
+// (Measured alternatives: try_wait with a suspend-time hint, one polling warp per
+// pipeline -- none faster.)
+// Iteration-bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// Each mbarrier.try_wait suspends the warp for up to a hardware time limit while the phase
+// is incomplete, so 2^30 iterations far exceed any legitimate wait; a poll iteration is ~4
+// instructions (the former clock-bounded loop read the clock with 64-bit arithmetic in
+// every iteration, ptxas hoisting clock64() above its k % 64 test: same speed, measured).
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
-    if (mbar_try_wait(b, phase)) return;
-    const long long t0 = clock64();
-    for (uint32_t k = 1;; ++k) {
-        if (mbar_try_wait(b, phase)) return;
-        if ((k & 63u) == 0 && clock64() - t0 > (1ll << 34)) __trap();   // ~9 s at 1.9 GHz
-    }
+    for (uint32_t k = 0; !mbar_try_wait(b, phase); ++k)
+        if (k == (1u << 30)) __trap();
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
