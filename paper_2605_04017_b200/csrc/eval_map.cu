@@ -97,12 +97,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t phase) {
 // pipeline -- none faster.)
 // Iteration-bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
 // Each mbarrier.try_wait suspends the warp for up to a hardware time limit while the phase
-// is incomplete, so 2^30 iterations far exceed any legitimate wait; a poll iteration is ~4
+// is incomplete, so 2^26 iterations (~1 s .. 1 min) far exceed any legitimate wait (< 1 ms); a poll iteration is ~4
 // instructions (the former clock-bounded loop read the clock with 64-bit arithmetic in
 // every iteration, ptxas hoisting clock64() above its k % 64 test: same speed, measured).
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
     for (uint32_t k = 0; !mbar_try_wait(b, phase); ++k)
-        if (k == (1u << 30)) __trap();
+        if (k == (1u << 26)) __trap();
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
