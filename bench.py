@@ -138,9 +138,9 @@ def bind_numa_local(dev: int) -> str:
         h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
         words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
         cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
-        cpus &= set(range(os.cpu_count()))
+        cpus &= set(os.sched_getaffinity(0))   # within the cores this process may use
         if not cpus:
-            return "cpu affinity: none reported"
+            return "cpu affinity unchanged (no GPU-local core available)"
         os.sched_setaffinity(0, cpus)
         return f"bound to the {len(cpus)} cores local to the GPU"
     except Exception as ex:   # no NVML / no affinity support: keep the default placement
