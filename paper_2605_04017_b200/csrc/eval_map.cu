@@ -19,11 +19,15 @@
 //    would exceed the 2e-3 output tolerance (SURVEY [B3]);
 //  * biases are folded into the contraction (bf16 hi/mid/lo bias columns in B times a
 //    constant ones A tile shared by all groups in shared memory); epilogue per layer:
-//    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> warp 0 issues the
-//    next layer's MMAs (the 16 most logit-influential units of the classifier's first
-//    hidden layer -- ordered first at map load, map.cpp -- use an accurate rational tanh
-//    instead of tanh.approx);
-//  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs;
+//    tcgen05.ld -> tanh -> split -> tcgen05.st -> named barrier -> warp (g mod 4) of
+//    group g issues the next layer's MMAs (the 16 most logit-influential units of the
+//    classifier's first hidden layer -- ordered first at map load, map.cpp -- use an
+//    accurate rational tanh instead of tanh.approx);
+//    the regressor's 6-wide output layer is one more MMA round (N = 16), the classifier's
+//    single output an fp32 dot product;
+//  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs; the tile
+//    claim and the staging are done by warp ((g + 2) mod 4) -- single-warp duties spread
+//    over the four SM sub-partitions (warp q of every group runs on sub-partition q);
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
 //    memory; the regressor only runs on full 128-row tiles of queued rays (plus one
 //    final partial flush), so its tensor and MUFU work scales with the valid fraction.
