@@ -88,3 +88,44 @@ def test_flare_film_sharding_is_exact(gpu_lib):
     half = n // 2
     assert np.array_equal(film_of(0, half) + film_of(half, half), whole)
     assert whole.sum() > 0
+
+
+@pytest.mark.parametrize("name,prec", [("C2", 0), ("C3", 0), ("C3", 1)])
+def test_results_do_not_depend_on_the_compaction_point(gpu_lib, tmp_path, name, prec):
+    """The block compaction only moves rays between lanes: moving it
+    (PLT_TRACE_SPLIT_DELTA, read when a path program is compiled -- so in a subprocess) leaves
+    every output bit, mask bit and guard-band flag unchanged, fp32 (JIT) and fp64."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    plt = gpu_lib
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "moved.npz"
+    n = (1 << 17) + 3
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, torch
+import paper_2605_04017_b200 as plt
+from plt_inputs import configs as C, rays as R
+cfg = C.CONFIGS[{name!r}]
+lens = plt.Lens(C.lens_text({name!r}), **cfg["opts"])
+d = plt.rays_to_device(R.gen_rays(cfg["law"], 29, 0, {n}))
+h = plt.alloc_hits({n}, flags=True)
+plt.trace_rays(lens, lens.all_t_id(), d, h, direction=cfg["direction"], precision={prec})
+torch.cuda.synchronize()
+np.savez({str(out)!r}, **{{k: h[k].cpu().numpy() for k in plt.HIT_KEYS + ("mask_bits", "flags")}})
+"""
+    for delta in ("-3", "1"):
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, PLT_TRACE_SPLIT_DELTA=delta),
+                       timeout=600)
+        g = np.load(out)
+        cfg = C.CONFIGS[name]
+        lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+        d = plt.rays_to_device(R.gen_rays(cfg["law"], 29, 0, n))
+        h = plt.alloc_hits(n, flags=True)
+        plt.trace_rays(lens, lens.all_t_id(), d, h, direction=cfg["direction"], precision=prec)
+        torch.cuda.synchronize()
+        for k in plt.HIT_KEYS + ("mask_bits", "flags"):
+            a = h[k].cpu().numpy()
+            assert np.array_equal(a.view(np.uint8), g[k].view(np.uint8)), (delta, k)
