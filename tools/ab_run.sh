@@ -1,19 +1,22 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
-o=gpurun_out/ab30
-for r in 1 2; do
-  timeout 120 python tools/trace_time_probe.py --config C3 --rays 67108864 --tag back-2 >> $o.jsonl 2>&1
-  PLT_TRACE_SPLIT_DELTA=2 timeout 120 python tools/trace_time_probe.py --config C3 --rays 67108864 --tag stop >> $o.jsonl 2>&1
-  timeout 120 python tools/trace_time_probe.py --config C3 --rays 67108864 --fp64 --tag back-2 >> $o.jsonl 2>&1
-  PLT_TRACE_SPLIT_DELTA=2 timeout 120 python tools/trace_time_probe.py --config C3 --rays 67108864 --fp64 --tag stop >> $o.jsonl 2>&1
-  timeout 120 python tools/trace_time_probe.py --config C2 --tag fwd >> $o.jsonl 2>&1
+o=gpurun_out/ab33
+for v in base both; do
+  case $v in base) D="";; both) D="#define PLT_TRACE_COST_FAST 1
+#define PLT_TRACE_T1_FAST 1";; esac
+  PLT_JIT_DEFINES="$D" timeout 900 python -m pytest tests/test_gpu_trace.py tests/test_gpu_full_range.py tests/test_gpu_fuzz_lenses.py -q -s -k "c1_ or c2_ or c3_ or ragged or full_range or fuzz" 2>&1 | grep -E "^compare_trace|passed|failed" | sed "s/^/$v /" >> $o.log
 done
-timeout 900 python -m pytest tests/test_gpu_trace.py tests/test_gpu_camera.py tests/test_gpu_full_range.py tests/test_gpu_unit_dirs.py tests/test_gpu_asphere.py -q > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
 python - <<'PY'
-import json
-for l in open("gpurun_out/ab30.jsonl"):
-    if l.startswith("{"):
-        d = json.loads(l); print(d["tag"], d["config"], d["fp64"], round(d["ms"], 4))
-    else: print(l[:200])
+import ast, collections
+mx = collections.defaultdict(lambda: {'max_dp':0,'max_dw':0,'max_dI':0, 'n':0})
+for l in open("gpurun_out/ab33.log"):
+    v, rest = l.split(" ", 1)
+    if rest.startswith("compare_trace"):
+        d = ast.literal_eval(rest[len("compare_trace "):].strip())
+        if d.get("n", 0) >= 4096:
+            m = mx[v]
+            for k in ('max_dp','max_dw','max_dI'): m[k] = max(m[k], d.get(k, 0))
+            m['n'] += 1
+    else: print(v, rest.strip())
+for v, m in mx.items(): print(v, m)
 PY
-tail -n 2 $o.tests.log
