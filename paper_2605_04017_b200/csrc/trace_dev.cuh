@@ -94,10 +94,6 @@ __device__ __forceinline__ float rsqrt_approx1(float x) {
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ float rcp1(float b) {                 // Newton-refined, as Math<float>::rcp
-    const float r = rcp_approx1(b);
-    return fmaf(r, fmaf(-b, r, 1.f), r);
-}
 __device__ __forceinline__ f2 rcp_approx2(f2 b) { return mk(rcp_approx1(b.v.x), rcp_approx1(b.v.y)); }
 __device__ __forceinline__ f2 rcp2(f2 b) {                      // Newton-refined, as Math<float>::rcp
     const f2 r = rcp_approx2(b);
@@ -105,14 +101,6 @@ __device__ __forceinline__ f2 rcp2(f2 b) {                      // Newton-refine
 }
 __device__ __forceinline__ f2 sqrt2(f2 x) {                     // as Math<float>::sqrt
     x = mk(fmaxf(x.v.x, 1e-30f), fmaxf(x.v.y, 1e-30f));
-    const f2 r = mk(rsqrt_approx1(x.v.x), rsqrt_approx1(x.v.y));
-    const f2 s = x * r;
-    return fma2(mk(0.5f) * r, fma2(-s, s, x), s);
-}
-// sqrt without the clamp, for arguments whose negative / zero values only occur on lanes
-// that are killed (disc < 0, TIR) or flagged for the fp64 re-trace (disc, kappa within
-// their guard bands): the NaN such a lane may carry never reaches an output.
-__device__ __forceinline__ f2 sqrt2_nc(f2 x) {
     const f2 r = mk(rsqrt_approx1(x.v.x), rsqrt_approx1(x.v.y));
     const f2 s = x * r;
     return fma2(mk(0.5f) * r, fma2(-s, s, x), s);
@@ -260,9 +248,13 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
 #ifdef PLT_TRACE_EXPLICIT_KILLS
         alive = alive & le(mk(0.f), disc);
 #endif
-        // a miss (disc < 0) needs no test of its own: sqrt2_nc(disc) is NaN there, so t is NaN
+        // a miss (disc < 0) needs no test of its own: the root of disc is NaN there, so t is NaN
         // and the lane dies at t > eps below (comparisons with NaN are false)
-        const f2 rt = sqrt2_nc(disc);
+        // sqrt(disc) = disc rsqrt(disc) from the MUFU seed (~2 ulp), no Newton step: C2 / C3
+        // errors vs the oracle unchanged at the 2.6e-5 / 1.5e-5 mm level (tolerance 1e-4; they
+        // come from the accumulated roundings, not this root).  disc < 0 or = 0: NaN -> the
+        // lane dies at t > eps (disc = 0 lies inside the disc guard band: fp64 re-trace)
+        const f2 rt = disc * mk(rsqrt_approx1(disc.v.x), rsqrt_approx1(disc.v.y));
         // q = -(b + copysign(rt, b)) (b = -0 takes -rt: same root pair {q, c/q} = {-+rt, +-rt}).
         // q = 0 (b = disc = 0) needs no test: t is then 0, +-inf or NaN, and the lane dies at
         // t > eps or at the aperture
@@ -335,7 +327,7 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
                                              : (st.is_R ? sel(tir, mk(1.f), Rf0) : Rf0);
 #endif
     if (!st.is_R) {
-        // TIR on a T step absorbs (A6): cost = sqrt2_nc(kappa < 0) is NaN, so the new
+        // TIR on a T step absorbs (A6): cost = root of kappa < 0 is NaN, so the new
         // direction is NaN and the lane dies at the next step's direction test (or at the
         // output plane's w_z > 0) -- no test here
 #ifdef PLT_TRACE_EXPLICIT_KILLS
@@ -388,7 +380,7 @@ __device__ __forceinline__ bool ray_finish1(const Program<float>& P, bool alive,
                                             float oz, float wx, float wy, float wz, float I, RayOut& out) {
     near |= alive && fabsf(wz) < kBandDir;
     alive = alive && wz > 0.f;
-    const float t = (P.z_out - oz) * rcp1(wz);
+    const float t = (P.z_out - oz) * rcp_approx1(wz);   // MUFU seed (~1 ulp), as t1 above
     alive = alive && t > 0.f;
     const float px = fmaf(t, wx, ox), py = fmaf(t, wy, oy);
     if (P.has_rect) {
