@@ -135,14 +135,18 @@ __device__ __forceinline__ void ray_init2(const Program<float>& P, Ray2& r, m2 a
     if (P.flip) { wz = -wz; plane_z = P.z_mirror - plane_z; }
     r.ox = ox; r.oy = oy; r.oz = mk(plane_z);
     if (complete) {
-        r.wx = wx; r.wy = wy; r.wz = sqrt2(fma2(-wx, wx, fma2(-wy, wy, mk(1.f))));
+        // w_z = sqrt(max(1 - w_x^2 - w_y^2, 1e-30)) from the MUFU rsqrt seed (~2 ulp; the fp32
+        // pass takes no Newton steps)
+        const f2 m = fma2(-wx, wx, fma2(-wy, wy, mk(1.f)));
+        const f2 mc = mk(fmaxf(m.v.x, 1e-30f), fmaxf(m.v.y, 1e-30f));
+        r.wx = wx; r.wy = wy; r.wz = mc * mk(rsqrt_approx1(mc.v.x), rsqrt_approx1(mc.v.y));
     } else {
         const f2 inv = rsqrt2(fma2(wx, wx, fma2(wy, wy, wz * wz)));
         r.wx = wx * inv; r.wy = wy * inv; r.wz = wz * inv;
     }
     const f2 lum = lam_nm * mk(1e-3f);
     r.l2 = lum * lum;
-    r.u = rcp2(r.l2);
+    r.u = rcp_approx2(r.l2);   // 1/lambda^2 (MUFU seed): feeds the eta polynomial / glass formulas
     r.I = mk(1.f); r.ncur = mk(1.f);
     r.alive = alive; r.near = {false, false};
 }
@@ -481,7 +485,7 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
                 if (!own.y) { lam.v.y = 550.f; r.wz.v.y = 1.f; }   // idle lane: harmless finite state
                 const f2 lum = lam * mk(1e-3f);
                 r.l2 = lum * lum;
-                r.u = rcp2(r.l2);
+                r.u = rcp_approx2(r.l2);
                 r.near = m2{(code.x & 0x10000) != 0, own.y && (code.y & 0x10000) != 0};
                 slot_x = code.x & 0xFFFF;
                 slot_y = own.y ? (code.y & 0xFFFF) : 0;
