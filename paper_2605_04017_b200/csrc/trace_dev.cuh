@@ -187,9 +187,11 @@ constexpr float kEtaU0 = 4.3f, kEtaUS = 1.f / 2.7f;   // u in [1.6, 7.0] (lambda
 // kN1 (JIT only): the ray is in air before this step, so ncur == 1 exactly and the
 // products with it are dropped (the packed intrinsics are opaque to constant folding).
 template <bool kAsph, class PP, bool kN1 = false, class EP = NoEta>   // PP: Program<float>, or the JIT's header
+// rho2o: x^2 + y^2 of the ray's origin (the previous step's hit, computed by its aperture
+// test), kept by the caller across steps.
 __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox, f2& oy, f2& oz,
                                       f2& wx, f2& wy, f2& wz, f2& I, f2& ncur, const f2 u, const f2 l2,
-                                      m2& alive, m2& near, const EP& ep = EP{}, const f2 v = f2{}) {
+                                      m2& alive, m2& near, f2& rho2o, const EP& ep = EP{}, const f2 v = f2{}) {
     // O4 direction sanity
     near = near | (alive & lt(abs2(wz), mk(kBandDir)));
 #ifdef PLT_JIT   // constant program: the sign test and the air shortcut below fold at compile time
@@ -242,13 +244,14 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
         t = -lz * rcp2(wz);
     } else {
         const f2 b = fma2(ox, wx, fma2(oy, wy, (lz - mk(st.R)) * wz));
-        const f2 c = fma2(ox, ox, fma2(oy, oy, lz * (lz - mk(st.twoR))));
+        const f2 c = fma2(lz, lz - mk(st.twoR), rho2o);   // |o'|^2 - R^2 (vertex-local origin)
         const f2 disc = fma2(b, b, -c);
         // guard band on |disc| scaled by |o'|^2 + R^2 = c + R (2 lz + R): the float32 rounding
         // of b^2 - c is ~eps (|o'| + |R|)^2 for hits and near-tangent misses alike (a band
         // relative to b^2 alone under-covers rays whose closest approach is near their
         // origin; the band used to cover every miss instead, re-tracing ~37 % of C3's rays)
-        near = near | (alive & lt(abs2(disc), mk(kBandDisc) * (c + mk(st.R) * fma2(lz, mk(2.f), mk(st.R)))));
+        near = near | (alive & lt(abs2(disc), fma2(lz, mk(kBandDisc * 2.f * st.R),
+                                                   fma2(c, mk(kBandDisc), mk(kBandDisc * st.R * st.R)))));
 #ifdef PLT_TRACE_EXPLICIT_KILLS
         alive = alive & le(mk(0.f), disc);
 #endif
@@ -278,6 +281,7 @@ __device__ __forceinline__ void step2(const Step<float>& st, const PP& P, f2& ox
     ox = fma2(t, wx, ox); oy = fma2(t, wy, oy); oz = fma2(t, wz, oz);
     // O6 clear aperture / stop / housing
     const f2 rho2 = fma2(ox, ox, oy * oy);
+    rho2o = rho2;
     near = near | (alive & lt(abs2(rho2 - mk(st.a2)), mk(st.band_a)));
     alive = alive & le(rho2, mk(st.a2));
     if (P.has_housing) {
@@ -358,9 +362,10 @@ template <bool kAsph>
 __device__ __forceinline__ void ray_steps2(const Program<float>& P, Ray2& r, int s0, int s1) {
     f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;
     m2 alive = r.alive, near = r.near;
+    f2 rho2o = fma2(ox, ox, oy * oy);
     for (int s = s0; s < s1; ++s) {
         if (!__any_sync(0xffffffffu, any2(alive))) break;
-        step2<kAsph>(P.st[s], P, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near);
+        step2<kAsph>(P.st[s], P, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near, rho2o);
     }
     r.ox = ox; r.oy = oy; r.oz = oz; r.wx = wx; r.wy = wy; r.wz = wz; r.I = I; r.ncur = ncur;
     r.alive = alive; r.near = near;

@@ -201,10 +201,10 @@ std::string gen_phase(const Program<float>& P, int s0, int s1, const std::vector
             c += "              constexpr EtaPoly<" + std::to_string(e.size() - 1) + "> ep{{";
             for (size_t k = 0; k < e.size(); ++k) c += lit(e[k]) + (k + 1 < e.size() ? ", " : "");
             c += "}};\n              step2<true, Hdr, " + std::string(n1) + ", EtaPoly<" + std::to_string(e.size() - 1) +
-                 ">>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near, ep, v); }\n";
+                 ">>(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near, rho2o, ep, v); }\n";
         } else {
             c += "              step2<true, Hdr, " + std::string(n1) +
-                 ">(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near); }\n";
+                 ">(st, H, ox, oy, oz, wx, wy, wz, I, ncur, r.u, r.l2, alive, near, rho2o); }\n";
         }
     }
     c += "        } while (0);\n";
@@ -248,7 +248,8 @@ std::string gen_source(const Program<float>& P) {
            "        constexpr Hdr H{" + std::to_string(P.has_housing) + ", " + lit(P.housing2) + ", " + lit(P.band_h) +
            "};\n"
            "        f2 ox = r.ox, oy = r.oy, oz = r.oz, wx = r.wx, wy = r.wy, wz = r.wz, I = r.I, ncur = r.ncur;\n"
-           "        m2 alive = r.alive, near = r.near;\n";
+           "        m2 alive = r.alive, near = r.near;\n"
+           "        f2 rho2o = fma2(ox, ox, oy * oy);\n";
     if (!polys.empty()) {
         src += "        const f2 v = fma2(r.u, mk(kEtaUS), mk(-kEtaU0 * kEtaUS));\n";
         // rays outside the fitted wavelength range go to the exact float64 re-trace
