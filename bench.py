@@ -287,6 +287,13 @@ CONFIGS = ("C2", "C3", "C4_22", "C4_59", "C5")
 FP64_LANES_PER_SM = 64                             # B200 FP64 FMA lanes per SM (nominal; DESIGN.md roofline)
 
 
+with open(os.path.join(ROOT, "profiles", "trace_flops.json")) as _f:
+    _tf = json.load(_f)
+TRACE_FLOPS_STEP = _tf["flops_per_step"]          # per step kind (tools/trace_flops.py)
+TRACE_FLOPS_INIT = _tf["flops_per_step"]["init"]
+del _tf
+
+
 def trace_flops_table():
     """profiles/trace_flops.json: algorithmic FLOPs per ray per (config, path), written by
     tools/trace_flops.py from the oracle's step bookkeeping (a stored value; bench never runs
@@ -523,13 +530,19 @@ def run_plt(args, ws, rank, local):
         total = len(ghosts) * 3 * npc
         lo_q, hi_q = rank * total // ws, (rank + 1) * total // ws
         segs = []            # (ghost, channel, first ray, count) of this rank's flat range
-        q = lo_q
+        q = lo_q             # channel-major: a rank's ghosts of one channel share one trace_paths call
         while q < hi_q:
             item, i0 = divmod(q, npc)
-            g, c = ghosts[item // 3], item % 3
+            c, g = item // len(ghosts), ghosts[item % len(ghosts)]
             cnt = min(npc - i0, hi_q - q)
             segs.append((g, c, i0, cnt))
             q += cnt
+        # trace groups: segments over the same (channel, ray range) -> one plt_trace_paths call
+        # (fp64: the ghosts' common all-T prefix traced once, include/plt.h)
+        tgroups = {}
+        for g, c, i0, cnt in segs:
+            tgroups.setdefault((c, i0, cnt), []).append(g)
+        tgroups = [(c, i0, cnt, gs) for (c, i0, cnt), gs in tgroups.items()]
         h = plt.alloc_hits(npc, dev)
         film = torch.zeros(fd["channels"] * fd["height_px"] * fd["width_px"], dtype=torch.int64, device=dev)
         ev = Events(["trace_rays", "eval_map", "film_allreduce"], args.steps, stream)
@@ -545,12 +558,12 @@ def run_plt(args, ws, rank, local):
         def view(d, i0, cnt):
             return {k: (v[i0:i0 + cnt] if k != "plane_z" and v is not None else v) for k, v in d.items()}
 
-        def fan_out(phase, launch):
+        def fan_out(phase, launch, items):
             if len(sides) > 1:
                 fork_ev[phase].record(stream)
                 for sd in sides:
                     sd.wait_event(fork_ev[phase])
-            for j, seg in enumerate(segs):
+            for j, seg in enumerate(items):
                 launch(seg, sides[j % len(sides)], hs[j % len(sides)])
             if len(sides) > 1:
                 for sd, e in zip(sides, join_ev[phase]):
@@ -561,19 +574,19 @@ def run_plt(args, ws, rank, local):
             film.zero_()
             ev.mark(k, 0)
 
-            def tr(seg, sd, hh):
-                g, c, i0, cnt = seg
+            def tr(grp, sd, hh):
+                c, i0, cnt, gs = grp
                 spl = {"film_desc": fd, "film": film, "channel": chan_ids[c][i0:i0 + cnt], "weight_scale": 1.0 / npc}
-                plt.trace_rays(lens, g, view(chans[c], i0, cnt), hh, precision=plt.FP64, n=cnt, stream=sd,
-                               splat=spl)
+                plt.trace_paths(lens, gs, view(chans[c], i0, cnt), [hh] * len(gs), precision=plt.FP64, n=cnt,
+                                stream=sd, splat=spl)
 
             def mp(seg, sd, hh):
                 g, c, i0, cnt = seg
                 spl = {"film_desc": fd, "film": film, "channel": chan_ids[c][i0:i0 + cnt], "weight_scale": 1.0 / npc}
                 plt.eval_map(maps[g], view(chans[c], i0, cnt), hh, n=cnt, stream=sd, splat=spl)
-            fan_out(0, tr)
+            fan_out(0, tr, tgroups)
             ev.mark(k, 1)
-            fan_out(1, mp)
+            fan_out(1, mp, segs)
             ev.mark(k, 2)
             if dist is not None:
                 dist.all_reduce(film)
@@ -584,7 +597,16 @@ def run_plt(args, ws, rank, local):
             np.save(args.dump_film, film.cpu().numpy())
         per = {k: v / 1e3 for k, v in ev.per_step_ms().items()}
         n = hi_q - lo_q
-        fl = sum(flops_tab[name][str(g)]["flops_per_ray"] * cnt for g, c, i0, cnt in segs)
+        # algorithmic FLOPs of the shared-prefix trace (plt_trace_paths): per group, the all-T
+        # prefix up to the deepest first reflection once per ray, plus every ghost's own steps
+        # from its first reflection on (profiles/trace_flops.json, tools/trace_flops.py)
+        tab, allt = flops_tab[name], flops_tab[name][str(int(ids[0]))]
+        fl = 0.0
+        for c, i0, cnt, gs in tgroups:
+            dmax = max(tab[str(g)]["first_R_step"] for g in gs)
+            pre = TRACE_FLOPS_INIT + sum(a * TRACE_FLOPS_STEP[kd] for a, kd in
+                                         list(zip(allt["alive_before_step"], allt["steps"]))[:dmax])
+            fl += cnt * (pre + sum(tab[str(g)]["suffix_flops_per_ray"] for g in gs))
         # valid fraction of this rank's map queries (for the tanh count): re-run outside the timing
         vm_rays = 0
         for g, c, i0, cnt in segs:
@@ -593,18 +615,20 @@ def run_plt(args, ws, rank, local):
         v_map = vm_rays / max(n, 1)
         kernels = {
             "trace_rays": {"ms": per["trace_rays"] * 1e3, "M_rays_s": n / per["trace_rays"] / 1e6,
-                           "precision": "fp64 (binding for ghosts, A22)",
+                           "precision": "fp64 (binding for ghosts, A22)", "call": "plt_trace_paths per channel",
                            "roofline": dict(trace_roofline(fl, per["trace_rays"], sm_max, fp64=True),
                                             flops_per_ray=fl / max(n, 1))},
             "eval_map": {"ms": per["eval_map"] * 1e3, "M_rays_s": n / per["eval_map"] / 1e6, "valid_frac": v_map,
                          "roofline": map_roofline(n, v_map, per["eval_map"], sm_max)},
             "film_allreduce": {"ms": per["film_allreduce"] * 1e3, "bytes": film.numel() * 8},
         }
-        rays_per_rank, scaling, launches = n, "strong", 2 * len(segs)
+        # per trace group: the prefix kernel + (zero-fill, resume) per ghost; one eval_map per segment
+        rays_per_rank, scaling, launches = n, "strong", sum(1 + 2 * len(gs) for *_, gs in tgroups) + len(segs)
         dtype = "f64 trace, bf16xbf16->f32 map"
         cfg_line = {"workload": f"{name}: {'22 mm Nakamura @15 deg' if name == 'C4_22' else '59 mm double-Gauss @10 deg'} "
                                 f"flare image, {len(ghosts)} two-bounce ghosts x 3 channels x 2^20 rays "
-                                f"= {total:,} queries, each traced (fp64) and mapped ({fitted} fitted per-ghost maps, "
+                                f"= {total:,} queries, each traced (fp64; plt_trace_paths: the ghosts' common all-T "
+                                f"prefix traced once per channel) and mapped ({fitted} fitted per-ghost maps, "
                                 f"{len(ghosts) - fitted} seeded), splatted in-kernel into a 768x512x3 int64 film"
                                 + (", one NCCL film all-reduce per image" if ws > 1 else ""),
                     "rays_total": total, "rays_per_gpu": n, "lens": cfg["lens"], "ghosts": len(ghosts),

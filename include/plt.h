@@ -273,6 +273,30 @@ PLT_API plt_status plt_eval_map_splat(const plt_map* map, const plt_rays* in, co
                                       const plt_splat_target* splat, int64_t n, void* cuda_stream);
 
 /*
+ * Trace one ray batch along several paths of the same lens and direction -- the flare
+ * image's per-path forward loop (Listing 1: every ghost path traced from the
+ * same input rays).  Results are exactly those of one plt_trace_rays call per path
+ * (plt_trace_rays_splat when splat != NULL: every path splats into the one film), in
+ * order, on cuda_stream: path p's hits go to outs[p].
+ * PLT_FP64 shares the work the paths have in common: a path's steps before its first
+ * reflection are the all-T path's first steps (the same surfaces, interactions and
+ * media), so the batch is traced ONCE along the all-T program, the float64 state of the
+ * rays still alive before each path's first reflection is kept in device scratch, and each
+ * path resumes from its depth.  The state is the one the single-path kernel carries, so
+ * hits, masks and film are bit-identical to the per-path calls (a path whose prefix
+ * program differs, or the all-T path itself, is traced alone).  Scratch: 68 B per ray per
+ * distinct first-reflection depth (batches beyond 2 GiB of it run in chunks).  PLT_FP32
+ * traces each path with plt_trace_rays.
+ * path_ids: host, n_paths ids; outs: host array of n_paths plt_hits (device pointers).
+ * Errors: as plt_trace_rays for any path (ids validated before any device work), plus
+ * PLT_E_INVALID_ARG for n_paths < 0 or null path_ids / outs; n == 0 or n_paths == 0 is a
+ * no-op.
+ */
+PLT_API plt_status plt_trace_paths(const plt_lens* lens, const uint64_t* path_ids, int n_paths, plt_dir dir,
+                                   plt_precision prec, const plt_rays* in, const plt_hits* outs,
+                                   const plt_splat_target* splat, int64_t n, void* cuda_stream);
+
+/*
  * Inspection: the sm_100a cubin of the float32 trace kernel specialised for this path
  * program (the kernel plt_trace_rays launches for large batches; compiled with NVRTC, no
  * GPU needed).  Two-call pattern: *size receives the cubin size; the bytes are written

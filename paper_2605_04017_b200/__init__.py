@@ -16,7 +16,7 @@ import ctypes as C
 import math
 import os
 
-__all__ = ["load", "PltError", "Lens", "Map", "trace_rays", "eval_map", "splat_sensor", "film_resolve",
+__all__ = ["load", "PltError", "Lens", "Map", "trace_rays", "trace_paths", "eval_map", "splat_sensor", "film_resolve",
            "alloc_hits", "rays_to_device", "FORWARD", "BACKWARD", "FP32", "FP64", "LIB_PATH"]
 
 LIB_PATH = os.environ.get("PLT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libplt.so")
@@ -31,7 +31,7 @@ EXPORTED = ("plt_last_error", "plt_version", "plt_lens_load", "plt_lens_free", "
             "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat", "plt_eval_map_splat",
             "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted", "plt_shade_cards",
             "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays", "plt_query_host",
-            "plt_pupil_weight")
+            "plt_pupil_weight", "plt_trace_paths")
 
 
 class PltError(RuntimeError):
@@ -121,11 +121,12 @@ def load():
     L.plt_query_host.argtypes = [p, u64, i, i, p, p, p, p, p, p, i64, i64, p]
     L.plt_pupil_weight.argtypes = [d, d, d, p]
     L.plt_lens_pupils.argtypes = [p, d, p, p, p, p]
+    L.plt_trace_paths.argtypes = [p, p, i, i, i, p, p, p, i64, p]
     for f in ("plt_lens_load", "plt_lens_info", "plt_enumerate_ghosts", "plt_trace_rays", "plt_map_load",
               "plt_eval_map", "plt_splat_sensor", "plt_film_resolve", "plt_trace_rays_splat",
               "plt_eval_map_splat", "plt_trace_jit_cubin", "plt_shade_plane", "plt_shade_plane_weighted",
               "plt_shade_cards", "plt_propagate_rays", "plt_lens_pupils", "plt_trace_kernel", "plt_gen_rays",
-              "plt_query_host", "plt_pupil_weight"):
+              "plt_query_host", "plt_pupil_weight", "plt_trace_paths"):
         getattr(L, f).restype = st
     _lib = L
     return L
@@ -321,6 +322,23 @@ def trace_rays(lens: Lens, path_id: int, rays: dict, hits: dict, direction: int 
         t, _keep = _splat_struct(splat, n)
         _check(load().plt_trace_rays_splat(lens.handle, int(path_id), direction, precision, C.byref(r), C.byref(h),
                                            C.byref(t), n, _stream(stream)))
+
+
+def trace_paths(lens: Lens, path_ids, rays: dict, hits_list, direction: int = FORWARD, precision: int = FP32,
+                n: int | None = None, stream=None, splat: dict | None = None):
+    """plt_trace_paths: the batch traced along every path of `path_ids` (hits_list[p] gets path
+    p's hits) -- the same results as one trace_rays call per path; in float64 the paths'
+    common all-T prefix is traced once (include/plt.h)."""
+    n = _n_of(rays, n)
+    ids = [int(g) for g in path_ids]
+    if len(hits_list) != len(ids):
+        raise ValueError("need one hits dict per path")
+    r = _rays_struct(rays, n)
+    outs = (Hits * max(1, len(ids)))(*[_hits_struct(h, n) for h in hits_list])
+    arr = (C.c_uint64 * max(1, len(ids)))(*ids)
+    t, _keep = _splat_struct(splat, n) if splat is not None else (None, None)
+    _check(load().plt_trace_paths(lens.handle, arr, len(ids), direction, precision, C.byref(r), outs,
+                                  C.byref(t) if t is not None else None, n, _stream(stream)))
 
 
 def eval_map(m: Map, rays: dict, hits: dict, raw=None, n: int | None = None, stream=None, splat: dict | None = None):

@@ -191,6 +191,60 @@ static plt_status trace_impl(const plt_lens* lens, uint64_t path_id, plt_dir dir
     PLT_GUARD_END
 }
 
+plt_status plt_trace_paths(const plt_lens* lens, const uint64_t* path_ids, int n_paths, plt_dir dir,
+                           plt_precision prec, const plt_rays* in, const plt_hits* outs,
+                           const plt_splat_target* splat, int64_t n, void* cuda_stream) {
+    PLT_RANGE("plt_trace_paths");
+    PLT_GUARD_BEGIN
+    if (!lens) return set_err(PLT_E_INVALID_ARG, "lens is null");
+    if (dir != PLT_FORWARD && dir != PLT_BACKWARD) return set_err(PLT_E_INVALID_ARG, "bad direction");
+    if (prec != PLT_FP32 && prec != PLT_FP64) return set_err(PLT_E_INVALID_ARG, "bad precision");
+    if (n < 0) return set_err(PLT_E_INVALID_ARG, "n < 0");
+    if (n_paths < 0) return set_err(PLT_E_INVALID_ARG, "n_paths < 0");
+    if (n_paths > 0 && (!path_ids || !outs)) return set_err(PLT_E_INVALID_ARG, "null path_ids / outs");
+    std::vector<std::shared_ptr<plt::CompiledPath>> cps;
+    for (int p = 0; p < n_paths; ++p) cps.push_back(plt::compile_path(*lens, path_ids[p], (int)dir));
+    if (n == 0 || n_paths == 0) return PLT_OK;
+    if (!rays_ok(in)) return set_err(PLT_E_INVALID_ARG, "null ray pointer or non-finite plane z");
+    for (int p = 0; p < n_paths; ++p)
+        if (!hits_ok(&outs[p])) return set_err(PLT_E_INVALID_ARG, "null hit pointer in outs[" + std::to_string(p) + "]");
+    if (n >= (int64_t)1 << 31) return set_err(PLT_E_INVALID_ARG, "n must be < 2^31 per call");
+    plt::SplatCtx sc;
+    plt_status s = splat_target(splat, &sc);
+    if (s != PLT_OK) return s;
+    s = check_device();
+    if (s != PLT_OK) return s;
+    if (prec == PLT_FP32) {
+        for (int p = 0; p < n_paths; ++p) {
+            s = cuda_status(plt::launch_trace_fp32(cps[p]->pf, cps[p]->pd, *in, outs[p], n, cuda_stream, sc),
+                            "trace_paths(fp32)");
+            if (s != PLT_OK) return s;
+        }
+        return PLT_OK;
+    }
+    // the all-T program is the shared prefix; path p shares its steps [0, d_p), d_p = its
+    // first reflection, when those steps and the frame are the same bytes
+    auto pre = plt::compile_path(*lens, (uint64_t)1 << lens->n_optical, (int)dir);
+    const plt::Program<double>& A = pre->pd;
+    std::vector<const plt::Program<double>*> progs;
+    std::vector<int> depth;
+    for (int p = 0; p < n_paths; ++p) {
+        const plt::Program<double>& P = cps[p]->pd;
+        int d = 0;
+        while (d < P.n_steps && !P.st[d].is_R) ++d;
+        const bool same_frame = P.flip == A.flip && P.z_mirror == A.z_mirror && P.has_housing == A.has_housing &&
+                                P.housing2 == A.housing2 && P.has_asph == A.has_asph;
+        if (d >= P.n_steps || d > A.n_steps || !same_frame ||
+            std::memcmp(P.st, A.st, sizeof(plt::Step<double>) * (size_t)d) != 0)
+            d = 0;   // no reflection (all-T), or no common prefix: traced alone
+        progs.push_back(&P);
+        depth.push_back(d);
+    }
+    return cuda_status(plt::launch_trace_paths_fp64(A, progs, depth, *in, outs, n, cuda_stream, sc),
+                       "trace_paths(fp64)");
+    PLT_GUARD_END
+}
+
 plt_status plt_map_load(const plt_lens* lens, const void* blob, size_t len, plt_map** out) {
     PLT_GUARD_BEGIN
     if (!blob || !out) return set_err(PLT_E_INVALID_ARG, "blob and out must be non-null");

@@ -159,6 +159,16 @@ int launch_trace_fp32(const Program<float>& pf, const Program<double>& pd, const
                       const plt_hits& out, int64_t n, void* stream, const SplatCtx& sc);
 int launch_trace_fp64(const Program<double>& pd, const plt_rays& in, const plt_hits& out,
                       int64_t n, void* stream, const SplatCtx& sc);
+#ifndef PLT_JIT
+}  // namespace plt
+#include <vector>
+namespace plt {
+// plt_trace_paths in float64 (trace.cu): the paths share the all-T program `pre` up to step
+// depth[p] (0: traced alone); outs[p] receives path p's hits.
+int launch_trace_paths_fp64(const Program<double>& pre, const std::vector<const Program<double>*>& paths,
+                            const std::vector<int>& depth, const plt_rays& in, const plt_hits* outs, int64_t n,
+                            void* stream, const SplatCtx& sc);
+#endif
 // Run-time specialised packed trace kernel for P (trace_jit.cpp): cudaKernel_t or nullptr.
 void* trace_jit_kernel(const Program<float>& P);
 // plt_kernel_kind of the float32 kernel that runs P (trace.cu); *jit receives the JIT kernel.

@@ -9,7 +9,7 @@ channels or GPUs.  Orchestration only: every step runs in the library's kernels.
 """
 from __future__ import annotations
 
-from . import BACKWARD, FP32, FP64, eval_map, propagate_rays, shade_plane, trace_rays
+from . import BACKWARD, FP32, FP64, eval_map, propagate_rays, shade_plane, trace_paths, trace_rays
 
 
 def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict | None = None,
@@ -47,9 +47,24 @@ def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict
         for sd in sides:
             sd.wait_event(fork)
     j = 0
+    # traced paths that all splat into `film`: one plt_trace_paths call per channel (in
+    # float64 their common all-T prefix is traced once; same film bit for bit)
+    traced = [int(p) for p in path_ids if not (maps and maps.get(int(p)) is not None)]
+    shared = per_path is None and len(traced) > 1
+    if shared:
+        for c, rays in enumerate(channel_rays):
+            n = int(rays["ox"].numel())
+            sd, hh = sides[j % len(sides)], hs[j % len(sides)]
+            j += 1
+            spl = {"film_desc": film_desc, "film": film, "channel": chan[c], "weight_scale": weight_scale}
+            trace_paths(lens, traced, rays, [hh] * len(traced), direction=direction, precision=precision, n=n,
+                        stream=sd, splat=spl)
     for pid in path_ids:
         target = per_path[pid] if per_path is not None else film
         m = maps.get(int(pid)) if maps else None
+        if m is None and shared:
+            used.append((int(pid), "trace"))
+            continue
         for c, rays in enumerate(channel_rays):
             n = int(rays["ox"].numel())
             sd, hh = sides[j % len(sides)], hs[j % len(sides)]

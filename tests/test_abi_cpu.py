@@ -387,3 +387,31 @@ def test_jit_uses_the_toolkit_nvrtc_even_with_torch_loaded(plt):
     cubin = L.trace_jit_cubin(L.all_t_id())
     m = re.search(rb"Cuda compilation tools, release (\d+\.\d+)", cubin)
     assert m and m.group(1).decode() == release, (m.group(0) if m else None, release)
+
+
+def test_trace_paths_validates_then_fails_loudly(plt):
+    """plt_trace_paths: n_paths < 0, null ids / outs, a null hit pointer or an id inconsistent
+    with the lens are PLT_E_INVALID_ARG before any device work; n == 0 / n_paths == 0 are
+    no-ops; a valid call needs the GPU (PLT_E_CUDA)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = plt.load()
+    L = plt.Lens(LENSES["wide22"])
+    ids = [int(g) for g in L.enumerate_ghosts(2)[0]][:3]
+    arr = (C.c_uint64 * 3)(*ids)
+    fake = [C.c_void_p(4096 * (k + 1)) for k in range(8)]
+    rays = plt.Rays(*fake[:6], -5.0)
+    outs = (plt.Hits * 3)(*[plt.Hits(*fake[:7], None) for _ in range(3)])
+    call = lambda a, k, o, n, prec=1: lib.plt_trace_paths(L.handle, a, k, 0, prec, C.byref(rays), o, None, n, None)
+    assert call(arr, 3, outs, 10) == 6
+    assert call(arr, 3, outs, 10, prec=0) == 6
+    assert call(arr, 3, outs, 0) == 0
+    assert call(arr, 0, outs, 10) == 0
+    assert call(arr, -1, outs, 10) == 1
+    assert call(None, 3, outs, 10) == 1
+    assert call(arr, 3, None, 10) == 1
+    bad = (plt.Hits * 3)(*[plt.Hits(*fake[:7], None) for _ in range(2)], plt.Hits(None, *fake[1:7], None))
+    assert call(arr, 3, bad, 10) == 1
+    wrong = (C.c_uint64 * 3)(ids[0], 12345678901, ids[2])
+    assert call(wrong, 3, outs, 10) == 1

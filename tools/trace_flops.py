@@ -31,11 +31,12 @@ from plt_inputs import rays as R  # noqa: E402
 FLOPS = {"sphere": 77, "plane": 56, "stop": 13, "output": 6, "init": 9}
 
 
-def step_kinds(lens, path_id, direction):
-    """Kinds of the surface steps along a path in the traversal frame, then 'output'."""
+def step_kinds(lens, path_id, direction, first_r=False):
+    """Kinds of the surface steps along a path in the traversal frame, then 'output'
+    (first_r: also the index of the path's first reflection step, None for all-T)."""
     surfs = lens.surfaces if direction == oracle.FORWARD else mirrored(lens)
     seq = decode_path(path_id)
-    kinds, s, d, k = [], 0, +1, 0
+    kinds, s, d, k, fr = [], 0, +1, 0, None
     while 0 <= s < len(surfs):
         sf = surfs[s]
         if sf.is_stop:
@@ -44,18 +45,26 @@ def step_kinds(lens, path_id, direction):
             kinds.append("plane" if sf.R == 0.0 else "sphere")
             if seq[k] == "R":
                 d = -d
+                if fr is None:
+                    fr = len(kinds) - 1
             k += 1
         s += d
-    return kinds + ["output"]
+    return (kinds + ["output"], fr) if first_r else kinds + ["output"]
 
 
 def path_flops(lens, path_id, direction, rays):
     t = oracle.trace(lens, path_id, direction, rays, threads=oracle.host_threads())
-    kinds = step_kinds(lens, path_id, direction)
+    kinds, fr = step_kinds(lens, path_id, direction, first_r=True)
     st = t["steps"]
     alive = [float((st >= k + 1).mean()) for k in range(len(kinds))]
     f = FLOPS["init"] + sum(a * FLOPS[kd] for a, kd in zip(alive, kinds))
-    return {"flops_per_ray": f, "valid": float(t["valid"].mean()), "steps": kinds, "alive_before_step": alive}
+    out = {"flops_per_ray": f, "valid": float(t["valid"].mean()), "steps": kinds, "alive_before_step": alive}
+    if fr is not None:
+        # plt_trace_paths (fp64) shares steps [0, first_R) with the all-T path: the work left
+        # to the path itself is the steps from its first reflection on
+        out["first_R_step"] = fr
+        out["suffix_flops_per_ray"] = sum(a * FLOPS[kd] for a, kd in list(zip(alive, kinds))[fr:])
+    return out
 
 
 def main():
