@@ -75,6 +75,7 @@ struct Smem {
     alignas(8) uint64_t bar_mma[G];           // MMA complete
     alignas(8) uint64_t bar_in[G][2];         // input stage full
     uint32_t tmem_base;
+    int fl_head[G], fl_count[G];              // end of the tile loop: each pipeline's leftover queue
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -526,21 +527,31 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const float* outw = reinterpret_cast<const float*>(S.w + P.lay.out_off);
 
     int qhead = 0, qcount = 0;
-    // regressor over queue entries [qhead, qhead + rows), rows <= 128
-    auto run_regressor = [&](int rows) {
-        group_bar(g);   // publish queue entries written by other threads of the group
+    // regressor over queue entries [qhead, qhead + rows), rows <= 128; chunk >= 0: rows
+    // [128 chunk, 128 chunk + rows) of the CTA's pooled leftovers (the pipelines' queues
+    // concatenated in pipeline order, read in place)
+    auto run_regressor = [&](int rows, int chunk) {
+        if (chunk < 0) group_bar(g);   // publish queue entries written by other threads of the group
         PLT_CLK(g0);
         const bool live = t < rows;
-        const int slot = (qhead + t) & (kQueue - 1);
+        const GroupSmem* src = &Gs;
+        int slot = (qhead + t) & (kQueue - 1);
+        if (chunk >= 0 && live) {
+            int e = kTile * chunk + t, p = 0;
+#pragma unroll 1
+            while (p < G - 1 && e >= S.fl_count[p]) e -= S.fl_count[p++];
+            src = &S.g[p];
+            slot = (S.fl_head[p] + e) & (kQueue - 1);
+        }
         Canon k;
         int qi = 0;
         if (live) {
-            const int code = Gs.qi[slot];
+            const int code = src->qi[slot];
             qi = code & 0x7FFFFFFF;
             k.flip = code < 0;
 #pragma unroll
-            for (int d = 0; d < 4; ++d) k.x[d] = Gs.qx[d][slot];
-            k.c = Gs.qc[slot]; k.s = Gs.qs[slot];
+            for (int d = 0; d < 4; ++d) k.x[d] = src->qx[d][slot];
+            k.c = src->qc[slot]; k.s = src->qs[slot];
         } else {
 #pragma unroll
             for (int d = 0; d < 4; ++d) k.x[d] = 0.f;
@@ -592,8 +603,10 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             const int ch = (live && P.sc.channel) ? (int)P.sc.channel[qi] : 0;
             splat_warp(P.sc, Gs.wsum + 32 * q, live, ox, oy, dz_out, I_out, ch);
         }
-        qhead = (qhead + rows) & (kQueue - 1);
-        qcount -= rows;
+        if (chunk < 0) {
+            qhead = (qhead + rows) & (kQueue - 1);
+            qcount -= rows;
+        }
     };
 
     // tiles: the first G per CTA statically (tile = group id), then dynamically -- one
@@ -666,7 +679,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         qcount += total;
         const int next_tile = Gs.next_tile[it & 1];   // written before the group barrier above
         PLT_CLK(o5);
-        if (qcount >= kTile) run_regressor(kTile);
+        if (qcount >= kTile) run_regressor(kTile, -1);
 #ifdef PLT_MAP_PROFILE
         const long long o6 = clock64();
         ++pr_tiles; pr_in += o1 - o0; pr_outep += o3 - o2; pr_write += o4 - o3; pr_queue += o5 - o4;
@@ -674,7 +687,15 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
 #endif
         tile = next_tile;
     }
-    if (qcount > 0) run_regressor(qcount);
+    // Leftovers (< 128 rays per pipeline): pooled across the CTA and run as full tiles,
+    // chunk c by pipeline c mod G -- one or two regressor runs per CTA instead of G partial
+    // ones (per-row results do not depend on the tile a ray shares).
+    if (t == 0) { S.fl_head[g] = qhead; S.fl_count[g] = qcount; }
+    __syncthreads();
+    int pooled = 0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) pooled += S.fl_count[j];
+    for (int c = g; kTile * c < pooled; c += G) run_regressor(min(kTile, pooled - kTile * c), c);
 #ifdef PLT_MAP_PROFILE
     if (blockIdx.x == 0 && (t & 31) == 0 && g < 2) {
         const long long tot = clock64() - pr_t0;

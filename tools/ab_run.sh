@@ -1,23 +1,23 @@
 # Developer A/B on a GPU box (one call); see DESIGN.md for the recorded outcomes.
 set -u
-o=gpurun_out/ab40
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pipemix tools/pipe_mix_bench.cu && /tmp/pipemix > $o.pipemix.json 2>&1
-for r in 1 2 3; do
-  for lib in paper_2605_04017_b200/libplt.so variants/libplt_ef.so variants/libplt_el.so variants/libplt_efel.so; do
-    PLT_LIB=$lib timeout 120 python tools/map_time_probe.py >> $o.jsonl 2>&1
+o=gpurun_out/ab41
+for r in 1 2; do
+  for lib in variants/libplt_prev.so paper_2605_04017_b200/libplt.so; do
+    t=$(basename $lib .so)
+    PLT_LIB=$lib timeout 120 python tools/map_time_probe.py --tag $t >> $o.jsonl 2>&1
+    for n in 262144 1048576 4194304; do
+      PLT_LIB=$lib timeout 120 python tools/map_time_probe.py --map C4_22 --ghost 65616 --rays $n --tag $t >> $o.jsonl 2>&1
+      PLT_LIB=$lib timeout 120 python tools/map_time_probe.py --map C4_59 --ghost 16404 --rays $n --tag $t >> $o.jsonl 2>&1
+    done
   done
 done
-for lib in paper_2605_04017_b200/libplt.so variants/libplt_ef.so variants/libplt_el.so variants/libplt_efel.so; do
-  t=$(basename $lib .so)
-  PLT_LIB=$lib timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_read.sum \
-    -k regex:eval_map -c 2 --csv python tools/map_time_probe.py --tag $t > $o.ncu_$t.csv 2>&1
-done
+timeout 1200 python -m pytest tests/test_gpu_map_splat.py tests/test_gpu_fitted_maps.py tests/test_gpu_fused_splat.py tests/test_gpu_flare_render.py tests/test_gpu_edge_cases.py -q -x > $o.tests.log 2>&1; echo "exit $?" >> $o.tests.log
 python - <<'PY'
 import json, collections
 d = collections.defaultdict(list)
-for l in open("gpurun_out/ab40.jsonl"):
+for l in open("gpurun_out/ab41.jsonl"):
     if l.startswith("{"):
-        j = json.loads(l); d[j["tag"]].append(round(j["ms"], 4))
-for k, v in d.items(): print(k, v)
+        j = json.loads(l); d[(j["map"], j.get("ghost", 0), j["rays"], j["tag"])].append(round(j["ms"], 4))
+for k in sorted(d): print(k, d[k])
 PY
-cat $o.pipemix.json
+tail -n 2 $o.tests.log

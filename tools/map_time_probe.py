@@ -28,12 +28,17 @@ def main():
     ap.add_argument("--coherent", action="store_true",
                     help="sort the rays by input position (rows, then columns): a pixel-ordered batch "
                          "whose valid fraction varies coherently along the index range")
+    ap.add_argument("--ghost", type=int, default=0, help="(C4 configs) a ghost's fitted flare map and channel-1 rays")
     a = ap.parse_args()
     cfg = C.CONFIGS[a.map]
     lens = plt.Lens(C.lens_text(a.map), **cfg["opts"])
-    m = plt.Map(C.fitted_map_blob(a.map), lens=lens)
     n = a.rays
-    rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
+    if a.ghost:
+        m = plt.Map(open(os.path.join(ROOT, "maps", "flare", a.map, f"{a.ghost}.pltmap"), "rb").read(), lens=lens)
+        rays = C.flare_rays(a.map, 1, 0, n)
+    else:
+        m = plt.Map(C.fitted_map_blob(a.map), lens=lens)
+        rays = R.gen_rays(cfg["law"], cfg["seed"], 0, n)
     if a.coherent:
         import numpy as np
         order = np.lexsort((rays["ox"], np.round(rays["oy"], 1)))
@@ -58,7 +63,7 @@ def main():
     w = h["mask_bits"].view(torch.int32)
     valid = float(sum(bin(x & 0xFFFFFFFF).count("1") for x in w[:4096].tolist())) / (4096 * 32)
     ms = statistics.median(ts)
-    print(json.dumps({"tag": a.tag, "map": a.map, "coherent": a.coherent, "rays": n, "ms": ms, "M_rays_s": n / ms / 1e3,
+    print(json.dumps({"tag": a.tag, "map": a.map, "ghost": a.ghost, "coherent": a.coherent, "rays": n, "ms": ms, "M_rays_s": n / ms / 1e3,
                       "valid_sample": valid, "min_ms": min(ts)}), flush=True)
 
 
