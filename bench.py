@@ -20,7 +20,7 @@ Scaling is weak: each rank owns its own chunk-aligned slice of the global index 
   C3     805,306,368 backward camera rays (192x128 px x 32768 spp), generated on the
          device; strong scaling, each rank owns 128/N pixel rows; trace + map.
   C4_22 / C4_59  flare image: every ghost x 3 channels x 2^20 rays, fp64 trace + per-ghost
-         map, splatted in-kernel; strong scaling over contiguous (ghost, channel, ray)
+         map, splatted in-kernel; strong scaling over contiguous (channel, ghost, ray)
          ranges, one NCCL int64 film all-reduce per image.
   C5     the throughput sweep (--rays 2^20 .. 2^30 per GPU, device-generated), as C2.
 
@@ -294,6 +294,27 @@ TRACE_FLOPS_INIT = _tf["flops_per_step"]["init"]
 del _tf
 
 
+def flare_partition(ghosts, n_channels, npc, rank, ws):
+    """SURVEY §8(e) for the flare image: the (channel, ghost, ray) sequence -- channel-major,
+    so a rank's ghosts of one channel are consecutive -- cut into ws contiguous ranges.
+    Returns this rank's segments [(ghost, channel, first ray, count)] and its trace groups
+    [(channel, first ray, count, [ghosts])]: the segments over the same (channel, ray range),
+    traced by one plt_trace_paths call (fp64: the ghosts' common all-T prefix once)."""
+    total = len(ghosts) * n_channels * npc
+    lo_q, hi_q = rank * total // ws, (rank + 1) * total // ws
+    segs, q = [], lo_q
+    while q < hi_q:
+        item, i0 = divmod(q, npc)
+        c, g = item // len(ghosts), ghosts[item % len(ghosts)]
+        cnt = min(npc - i0, hi_q - q)
+        segs.append((g, c, i0, cnt))
+        q += cnt
+    groups = {}
+    for g, c, i0, cnt in segs:
+        groups.setdefault((c, i0, cnt), []).append(g)
+    return segs, [(c, i0, cnt, gs) for (c, i0, cnt), gs in groups.items()]
+
+
 def trace_flops_table():
     """profiles/trace_flops.json: algorithmic FLOPs per ray per (config, path), written by
     tools/trace_flops.py from the oracle's step bookkeeping (a stored value; bench never runs
@@ -508,7 +529,7 @@ def run_plt(args, ws, rank, local):
                     "parallelism": f"{ws} ranks x {rows // ws} pixel rows (strong scaling)"}
     else:
         # ---- flare image: every two-bounce ghost x 3 channels x 2^20 rays (strong scaling over
-        # (ghost, channel, ray) ranges), fp64 trace + per-ghost map, both splatted in-kernel,
+        # (channel, ghost, ray) ranges), fp64 trace + per-ghost map, both splatted in-kernel,
         # one NCCL int64 film all-reduce per image (Eq. 8) --------------------------
         cfg = C.CONFIGS[name]
         lens = plt.Lens(C.lens_text(name), **cfg["opts"])
@@ -528,21 +549,7 @@ def run_plt(args, ws, rank, local):
         chans = [plt.gen_rays(K[c], cfg["seed"] * 16 + c, 0, npc) for c in range(3)]
         chan_ids = [torch.full((npc,), c, dtype=torch.uint8, device=dev) for c in range(3)]
         total = len(ghosts) * 3 * npc
-        lo_q, hi_q = rank * total // ws, (rank + 1) * total // ws
-        segs = []            # (ghost, channel, first ray, count) of this rank's flat range
-        q = lo_q             # channel-major: a rank's ghosts of one channel share one trace_paths call
-        while q < hi_q:
-            item, i0 = divmod(q, npc)
-            c, g = item // len(ghosts), ghosts[item % len(ghosts)]
-            cnt = min(npc - i0, hi_q - q)
-            segs.append((g, c, i0, cnt))
-            q += cnt
-        # trace groups: segments over the same (channel, ray range) -> one plt_trace_paths call
-        # (fp64: the ghosts' common all-T prefix traced once, include/plt.h)
-        tgroups = {}
-        for g, c, i0, cnt in segs:
-            tgroups.setdefault((c, i0, cnt), []).append(g)
-        tgroups = [(c, i0, cnt, gs) for (c, i0, cnt), gs in tgroups.items()]
+        segs, tgroups = flare_partition(ghosts, 3, npc, rank, ws)
         h = plt.alloc_hits(npc, dev)
         film = torch.zeros(fd["channels"] * fd["height_px"] * fd["width_px"], dtype=torch.int64, device=dev)
         ev = Events(["trace_rays", "eval_map", "film_allreduce"], args.steps, stream)
@@ -596,7 +603,7 @@ def run_plt(args, ws, rank, local):
         if args.dump_film and rank == 0:
             np.save(args.dump_film, film.cpu().numpy())
         per = {k: v / 1e3 for k, v in ev.per_step_ms().items()}
-        n = hi_q - lo_q
+        n = sum(cnt for *_, cnt in segs)
         # algorithmic FLOPs of the shared-prefix trace (plt_trace_paths): per group, the all-T
         # prefix up to the deepest first reflection once per ray, plus every ghost's own steps
         # from its first reflection on (profiles/trace_flops.json, tools/trace_flops.py)
@@ -633,7 +640,7 @@ def run_plt(args, ws, rank, local):
                                 + (", one NCCL film all-reduce per image" if ws > 1 else ""),
                     "rays_total": total, "rays_per_gpu": n, "lens": cfg["lens"], "ghosts": len(ghosts),
                     "l2": "rays 3 x 2^20 x 24 B = 75 MB, re-read per ghost (L2-resident by design)",
-                    "parallelism": f"{ws} ranks x contiguous (ghost, channel, ray) ranges (strong scaling)"}
+                    "parallelism": f"{ws} ranks x contiguous (channel, ghost, ray) ranges (strong scaling)"}
         extra_cfg["segments_rank0"] = len(segs)
 
     # ---- one JSON line (max over ranks) ------------------------------------------------------

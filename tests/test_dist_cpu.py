@@ -77,3 +77,26 @@ def test_gloo_film_allreduce_matches_single_process(tmp_path):
     assert np.array_equal(f0, (fa + fb).reshape(-1))
     assert f0.sum() > 0
     assert not np.array_equal(np.load(tmp_path / "ox_0.npy"), np.load(tmp_path / "ox_1.npy"))
+
+
+@pytest.mark.parametrize("ws", [1, 2, 3, 4, 8])
+def test_flare_partition_covers_the_image_once(ws):
+    """bench.flare_partition: the ranks' segments tile the (channel, ghost,
+    ray) sequence exactly once, each rank's share is within one ray of total / ws, and every
+    trace group is one (channel, ray range) with the ghosts of its segments."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    ghosts, nch, npc = [11, 22, 33, 44, 55], 3, 1000
+    seen = np.zeros((nch, len(ghosts), npc), np.int32)
+    for r in range(ws):
+        segs, groups = bench.flare_partition(ghosts, nch, npc, r, ws)
+        total = sum(cnt for *_, cnt in segs)
+        assert abs(total - len(ghosts) * nch * npc / ws) <= 1
+        for g, c, i0, cnt in segs:
+            seen[c, ghosts.index(g), i0:i0 + cnt] += 1
+        assert sorted((g, c, i0, cnt) for c, i0, cnt, gs in groups for g in gs) == sorted(segs)
+        assert len({(c, i0, cnt) for c, i0, cnt, _ in groups}) == len(groups)
+        if ws == 1:
+            assert len(groups) == nch and all(gs == ghosts for *_, gs in groups)
+    assert (seen == 1).all()

@@ -52,9 +52,9 @@ def _bench(args, ranks, tmp_env=None):
 
 @pytest.mark.parametrize("cfg", ["C4_22", "C4_59"])
 def test_flare_image_two_ranks_equals_one_rank_bitwise(tmp_path, cfg):
-    """the flare image sharded over (ghost, channel, ray) ranges on two ranks
+    """the flare image sharded over (channel, ghost, ray) ranges on two ranks
     and all-reduced (int64 SUM, Eq. 8) is bit-identical to the one-rank image -- through the
-    product path (plt_trace_rays_splat fp64 + plt_eval_map_splat, bench.py --config)."""
+    product path (plt_trace_paths fp64 + plt_eval_map_splat, bench.py --config)."""
     import numpy as np
     f1, f2 = tmp_path / "one.npy", tmp_path / "two.npy"
     d1 = _bench(["--config", cfg, "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--dump-film", str(f1)], 1)
