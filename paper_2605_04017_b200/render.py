@@ -9,7 +9,7 @@ channels or GPUs.  Orchestration only: every step runs in the library's kernels.
 """
 from __future__ import annotations
 
-from . import BACKWARD, FP32, FP64, eval_map, propagate_rays, shade_plane, trace_paths, trace_rays
+from . import BACKWARD, FP32, FP64, eval_map, propagate_rays, shade_plane, splat_sensor, trace_paths, trace_rays
 
 
 def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict | None = None,
@@ -49,16 +49,28 @@ def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict
     j = 0
     # traced paths that all splat into `film`: one plt_trace_paths call per channel (in
     # float64 their common all-T prefix is traced once; same film bit for bit)
+    # (per_path films: the shared trace writes every path's hits, then one plt_splat_sensor per
+    # path and channel -- the film the fused splat would give, bit for bit)
     traced = [int(p) for p in path_ids if not (maps and maps.get(int(p)) is not None)]
-    shared = per_path is None and len(traced) > 1
+    shared = len(traced) > 1
     if shared:
+        ph = [alloc_hits(nmax, device=dev) for _ in traced] if per_path is not None else None
         for c, rays in enumerate(channel_rays):
             n = int(rays["ox"].numel())
             sd, hh = sides[j % len(sides)], hs[j % len(sides)]
             j += 1
-            spl = {"film_desc": film_desc, "film": film, "channel": chan[c], "weight_scale": weight_scale}
-            trace_paths(lens, traced, rays, [hh] * len(traced), direction=direction, precision=precision, n=n,
-                        stream=sd, splat=spl)
+            if per_path is None:
+                spl = {"film_desc": film_desc, "film": film, "channel": chan[c], "weight_scale": weight_scale}
+                trace_paths(lens, traced, rays, [hh] * len(traced), direction=direction, precision=precision, n=n,
+                            stream=sd, splat=spl)
+                continue
+            trace_paths(lens, traced, rays, ph, direction=direction, precision=precision, n=n, stream=sd)
+            for pid, hp in zip(traced, ph):
+                splat_sensor(film_desc, per_path[pid], hp, channel=chan[c], weight_scale=weight_scale, n=n, stream=sd)
+            if len(sides) > 1:   # the next channel may run on another stream: it reuses ph
+                e = torch.cuda.Event()
+                e.record(sd)
+                sides[j % len(sides)].wait_event(e)
     for pid in path_ids:
         target = per_path[pid] if per_path is not None else film
         m = maps.get(int(pid)) if maps else None
@@ -82,8 +94,9 @@ def render_flare(lens, path_ids, channel_rays, film_desc: dict, film, maps: dict
             e.record(sd)
             base.wait_event(e)
         # buffers used on the side streams stay reserved until those streams' work is done
+        extra = [t for hh in (ph or []) for t in hh.values() if torch.is_tensor(t)] if shared else []
         for sd in sides:
-            for t in [t for hh in hs for t in hh.values() if torch.is_tensor(t)] + chan:
+            for t in [t for hh in hs for t in hh.values() if torch.is_tensor(t)] + chan + extra:
                 t.record_stream(sd)
     return used
 

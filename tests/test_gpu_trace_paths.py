@@ -193,3 +193,36 @@ np.savez(sys.argv[1], film=film.cpu().numpy(), **{f"{k}{j}": h[k].cpu().numpy() 
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
     assert a["film"].sum() > 0
+
+
+def test_render_flare_per_path_films_through_trace_paths(gpu_lib):
+    """render_flare(per_path=...) traces the ghosts with one plt_trace_paths call per channel and
+    splats each path's hits into its own film (plt_splat_sensor); every film must equal the
+    per-path fused trace + splat bit for bit, and so must the summed image."""
+    import torch
+    from paper_2605_04017_b200.render import render_flare
+    plt = gpu_lib
+    name = "C4_59"
+    cfg = C.CONFIGS[name]
+    lens = plt.Lens(C.lens_text(name), **cfg["opts"])
+    ghosts = [int(g) for g in lens.enumerate_ghosts(2)[0][1:]][::3]
+    n = (1 << 14) + 9
+    rays = [plt.rays_to_device(C.flare_rays(name, c, 0, n)) for c in range(3)]
+    fd = cfg["film"]
+    npx = fd["channels"] * fd["height_px"] * fd["width_px"]
+    per = {g: torch.zeros(npx, dtype=torch.int64, device="cuda") for g in ghosts}
+    render_flare(lens, ghosts, rays, fd, None, per_path=per, weight_scale=1.0 / n)
+    whole = torch.zeros(npx, dtype=torch.int64, device="cuda")
+    render_flare(lens, ghosts, rays, fd, whole, weight_scale=1.0 / n)
+    h = plt.alloc_hits(n)
+    total = torch.zeros(npx, dtype=torch.int64, device="cuda")
+    for g in ghosts:
+        ref = torch.zeros(npx, dtype=torch.int64, device="cuda")
+        for c in range(3):
+            ch = torch.full((n,), c, dtype=torch.uint8, device="cuda")
+            plt.trace_rays(lens, g, rays[c], h, precision=plt.FP64,
+                           splat={"film_desc": fd, "film": ref, "channel": ch, "weight_scale": 1.0 / n})
+        torch.cuda.synchronize()
+        assert torch.equal(per[g], ref), g
+        total += ref
+    assert torch.equal(whole, total) and int(total.sum()) > 0
