@@ -126,14 +126,16 @@ inline SplatCtx make_splat_ctx(const plt_film_desc& fd, int64_t* film, const uin
     // expression of O11, for hits inside (or near) the film: each of cxf, hwf, sxf and the
     // three roundings contributes <= 2^-24 relative to a term of magnitude <= |c| s + 2
     // width (in px), i.e. <= ((|cx| + |cy|) max(sx, sy) + 5 max(width, height)) 2^-24 with
-    // headroom x2; never below the historical 2e-3 px.  Hits closer than this to a pixel
-    // edge take the double path, so the film stays bit-identical for any film size.
+    // headroom x2 (4.6e-4 px for the bench's 768-px film; the former fixed floor of 2e-3 px
+    // sent ~4x more hits -- 13 % of the trace's splatting warps -- down the double path).
+    // Hits closer than this to a pixel edge take the double path, so the film stays
+    // bit-identical for any film size.
     {
         const double s = fd.width_px / c.W > fd.height_px / c.H ? fd.width_px / c.W : fd.height_px / c.H;
         const double m = fd.width_px > fd.height_px ? fd.width_px : fd.height_px;
         const double ac = (c.cx < 0 ? -c.cx : c.cx) + (c.cy < 0 ? -c.cy : c.cy);
         const double g = 2.0 * (ac * s + 5.0 * m) * 5.9604644775390625e-8;
-        c.guard = (float)(g > 2e-3 ? g : 2e-3);
+        c.guard = (float)g;
     }
     return c;
 }
