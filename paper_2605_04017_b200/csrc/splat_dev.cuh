@@ -53,10 +53,27 @@ __device__ __forceinline__ int splat_key(const SplatCtx& c, float px, float py, 
     return -1;
 }
 
+// Lanes whose hits share a pixel found with __match_any_sync; the lowest lane sums the
+// group's weights through `wsm` (this warp's 32 shared-memory slots) and issues ONE 64-bit
+// atom.add per distinct pixel per warp.  All 32 lanes call it.
+__device__ __forceinline__ void splat_aggregate(const SplatCtx& c, long long* wsm, int key, long long w) {
+    const int lane = threadIdx.x & 31;
+    wsm[lane] = w;
+    __syncwarp();
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && lane == __ffs(peers) - 1) {
+        long long sum = 0;
+        for (unsigned p = peers; p; p &= p - 1) sum += wsm[__ffs(p) - 1];
+        atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)sum);
+    }
+    __syncwarp();
+}
+
 // Warp-synchronous splat: ALL 32 lanes call it (hit = false for lanes without a valid
-// hit).  Lanes whose hits share a pixel find each other with __match_any_sync; the lowest
-// lane sums the group's weights through `wsm` (this warp's 32 shared-memory slots) and
-// issues ONE 64-bit atom.add per distinct pixel per warp.
+// hit).  Aggregate only where it pays: if no two neighbouring lanes share a pixel (a
+// spread-out image: the warp's hits almost surely land on 32 distinct pixels) every lane
+// adds its own weight; otherwise (a bright spot) lanes with the same pixel are grouped and
+// summed first.  Integer adds: the film is the same either way.
 __device__ __forceinline__ void splat_warp(const SplatCtx& c, long long* wsm, bool hit, float px, float py,
                                            float dz, float I, int ch) {
     const int lane = threadIdx.x & 31;
@@ -64,25 +81,42 @@ __device__ __forceinline__ void splat_warp(const SplatCtx& c, long long* wsm, bo
     long long w = 0;
     bool drop = false;
     if (hit) key = splat_key(c, px, py, dz, I, ch, w, drop);
-    // Aggregate only where it pays: if no two neighbouring lanes share a pixel (a spread-out
-    // image: the warp's hits almost surely land on 32 distinct pixels) every lane adds its
-    // own weight; otherwise (a bright spot) lanes with the same pixel are grouped with
-    // __match_any_sync and summed first.  Integer adds: the film is the same either way.
     const int nb = __shfl_down_sync(0xffffffffu, key, 1);
     if (!__any_sync(0xffffffffu, lane < 31 && key >= 0 && key == nb)) {
         if (key >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)w);
     } else {
-        wsm[lane] = w;
-        __syncwarp();
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        if (key >= 0 && lane == __ffs(peers) - 1) {
-            long long sum = 0;
-            for (unsigned p = peers; p; p &= p - 1) sum += wsm[__ffs(p) - 1];
-            atomicAdd(reinterpret_cast<unsigned long long*>(c.film + key), (unsigned long long)sum);
-        }
+        splat_aggregate(c, wsm, key, w);
     }
     const unsigned dm = __ballot_sync(0xffffffffu, drop);
     if (c.dropped && lane == 0 && dm) atomicAdd(c.dropped, (unsigned long long)__popc(dm));
+    __syncwarp();
+}
+
+// Two hits per lane (the packed trace's ray pair) in one warp-synchronous pass: the
+// neighbour test, the vote and the drop count are shared by both hits (half the warp-level
+// instructions of two splat_warp calls); the atomics are the same, so is the film.
+__device__ __forceinline__ void splat_warp2(const SplatCtx& c, long long* wsm, bool hit0, float px0, float py0,
+                                            float dz0, float I0, int ch0, bool hit1, float px1, float py1,
+                                            float dz1, float I1, int ch1) {
+    const int lane = threadIdx.x & 31;
+    int k0 = -1, k1 = -1;
+    long long w0 = 0, w1 = 0;
+    bool d0 = false, d1 = false;
+    if (hit0) k0 = splat_key(c, px0, py0, dz0, I0, ch0, w0, d0);
+    if (hit1) k1 = splat_key(c, px1, py1, dz1, I1, ch1, w1, d1);
+    const int nb0 = __shfl_down_sync(0xffffffffu, k0, 1), nb1 = __shfl_down_sync(0xffffffffu, k1, 1);
+    const bool clash = lane < 31 && ((k0 >= 0 && k0 == nb0) || (k1 >= 0 && k1 == nb1));
+    if (!__any_sync(0xffffffffu, clash)) {
+        if (k0 >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(c.film + k0), (unsigned long long)w0);
+        if (k1 >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(c.film + k1), (unsigned long long)w1);
+    } else {
+        splat_aggregate(c, wsm, k0, w0);
+        splat_aggregate(c, wsm, k1, w1);
+    }
+    if (c.dropped) {
+        const int nd = __popc(__ballot_sync(0xffffffffu, d0)) + __popc(__ballot_sync(0xffffffffu, d1));
+        if (lane == 0 && nd) atomicAdd(c.dropped, (unsigned long long)nd);
+    }
     __syncwarp();
 }
 

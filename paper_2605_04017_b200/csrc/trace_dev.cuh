@@ -519,8 +519,8 @@ __device__ __forceinline__ void trace_x2_body(const Program<float>& P, const plt
         if (sc.film) {   // fused splat; guard-band rays are splatted by the fp64 refine instead
             const int cx = (own.x && sc.channel) ? (int)sc.channel[ix] : 0;
             const int cy = (own.y && sc.channel) ? (int)sc.channel[iy] : 0;
-            splat_warp(sc, sm_w + 32 * warp, own.x && vx && !nx, ox_.px, ox_.py, ox_.dz, ox_.I, cx);
-            splat_warp(sc, sm_w + 32 * warp, own.y && vy && !ny, oy_.px, oy_.py, oy_.dz, oy_.I, cy);
+            splat_warp2(sc, sm_w + 32 * warp, own.x && vx && !nx, ox_.px, ox_.py, ox_.dz, ox_.I, cx,
+                        own.y && vy && !ny, oy_.px, oy_.py, oy_.dz, oy_.I, cy);
         }
         if (compact) {
             pending = base;
