@@ -25,9 +25,10 @@
 //    accurate rational tanh instead of tanh.approx);
 //    the regressor's 6-wide output layer is one more MMA round (N = 16), the classifier's
 //    single output an fp32 dot product;
-//  * ray inputs for tile k+1 are staged by cp.async.bulk (TMA) while tile k runs; the tile
-//    claim and the staging are done by warp ((g + 2) mod 4) -- single-warp duties spread
-//    over the four SM sub-partitions (warp q of every group runs on sub-partition q);
+//  * tiles go in pairs: the ray inputs of the next pair (two 128-ray tiles) are staged by
+//    cp.async.bulk (TMA) while the current pair runs; the pair claim and the staging are done
+//    by warp ((g + 2) mod 4) -- single-warp duties spread over the four SM sub-partitions
+//    (warp q of every group runs on sub-partition q);
 //  * gating: rays with logit >= 0 are appended to a per-group queue in shared
 //    memory; the regressor only runs on full 128-row tiles of queued rays (plus one
 //    final partial flush), so its tensor and MUFU work scales with the valid fraction.
@@ -53,18 +54,16 @@ constexpr int kOnesBytes = kTile * 16 * 2;    // 128 x 16 bf16, canonical K-majo
 constexpr int kNumIn = 5;                    // staged SoA inputs: ox, oy, dx, dy, lambda (dz unused)
 constexpr int kStageBytes = kNumIn * kTile * 4;
 constexpr uint32_t kMaxImageBytes = 20480;
-constexpr int kClaimChunk = 4;               // tiles per dynamic claim (one global atomic each)
 
 struct GroupSmem {
-    alignas(16) float stage[2][kNumIn][kTile];  // TMA-staged ray inputs
+    alignas(16) float stage[2][kNumIn][2 * kTile];  // TMA-staged ray inputs of a tile pair
     // queue of valid rays, kept with their canonical inputs so the regressor neither
     // gathers the inputs again nor re-canonicalises them (SoA: conflict-free)
     float qx[4][kQueue];                     // normalised canonical inputs x
     float qc[kQueue], qs[kQueue];            // rotation (cos, sin) to undo
     int qi[kQueue];                          // ray index | reflection flag << 31
     int wcount[4];                           // per-warp valid counts (prefix)
-    int next_tile[2];                        // dynamic scheduler: the group's next tile (by parity)
-    int chunk_next, chunk_left;              // the pipeline's claimed chunk of tiles: next, tiles left
+    int next_tile[2];                        // dynamic scheduler: the group's next tile pair (by parity)
     long long wsum[kTile];                   // fused splat: per-warp aggregation slots
 };
 
@@ -415,16 +414,19 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     const int n_tiles = (int)P.n_tiles;
     const int group_id = (int)blockIdx.x * G + g;
     const int group_stride = (int)gridDim.x * G;
-    auto tile_full_tma = [&](int tile) { return P.tma_ok && tile < n / kTile; };
-    auto issue_stage = [&](int tile, int st) {   // one thread of the group
+    // tile pairs: pair p = tiles 2p, 2p + 1, staged together (5 bulk copies of 1 KB per pair
+    // instead of 5 of 512 B per tile) when both tiles are full
+    const int n_pairs = (n_tiles + 1) / 2;
+    auto pair_full_tma = [&](int pr) { return P.tma_ok && 2 * pr + 1 < n / kTile; };
+    auto issue_pair = [&](int pr, int st) {   // one thread of the group
         fence_proxy_async();
-        mbar_expect_tx(&S.bar_in[g][st], kStageBytes);
-        const int o = tile * kTile;
-        tma_bulk_g2s(Gs.stage[st][0], P.in.ox + o, kTile * 4, &S.bar_in[g][st]);
-        tma_bulk_g2s(Gs.stage[st][1], P.in.oy + o, kTile * 4, &S.bar_in[g][st]);
-        tma_bulk_g2s(Gs.stage[st][2], P.in.dx + o, kTile * 4, &S.bar_in[g][st]);
-        tma_bulk_g2s(Gs.stage[st][3], P.in.dy + o, kTile * 4, &S.bar_in[g][st]);
-        tma_bulk_g2s(Gs.stage[st][4], P.in.lambda_nm + o, kTile * 4, &S.bar_in[g][st]);
+        mbar_expect_tx(&S.bar_in[g][st], 2 * kStageBytes);
+        const int o = pr * 2 * kTile;
+        tma_bulk_g2s(Gs.stage[st][0], P.in.ox + o, 2 * kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][1], P.in.oy + o, 2 * kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][2], P.in.dx + o, 2 * kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][3], P.in.dy + o, 2 * kTile * 4, &S.bar_in[g][st]);
+        tma_bulk_g2s(Gs.stage[st][4], P.in.lambda_nm + o, 2 * kTile * 4, &S.bar_in[g][st]);
     };
 
     const uint32_t w_base = smem_u32(S.w);
@@ -432,16 +434,17 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     uint32_t mma_phase = 0;
     uint32_t in_phase[2] = {0, 0};
 
-    int tile = group_id;
+    int pair = group_id, half = 0, pit = 0;
     // the per-tile duties (tile claim, input TMA) go to lane 0 of warp (g + 2) mod 4: neither
     // the MMA-issuing warp nor, for all pipelines, sub-partition 0
     const int duty_t = 32 * ((g + 2) & 3);
-    if (t == duty_t && tile < n_tiles && tile_full_tma(tile)) issue_stage(tile, 0);
+    if (t == duty_t && pair < n_pairs && pair_full_tma(pair)) issue_pair(pair, 0);
     mbar_wait(&S.bar_w, 0);
 
 #ifdef PLT_MAP_PROFILE
     long long pr_bar = 0, pr_issue = 0, pr_wait = 0, pr_epi = 0, pr_ld = 0, pr_tanh = 0, pr_st = 0, pr_fence = 0;
     long long pr_layers = 0, pr_ifence = 0, pr_immas = 0, pr_icommit = 0;
+    long long pr_lastbar = 0, pr_inbar = 0, pr_claim = 0, pr_top = 0;
     long long pr_tiles = 0, pr_in = 0, pr_outep = 0, pr_write = 0, pr_queue = 0, pr_reg = 0, pr_regs = 0, pr_gather = 0;
     const long long pr_t0 = clock64();
 #define PLT_CLK(v) const long long v = clock64()
@@ -449,7 +452,14 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
 #define PLT_CLK(v)
 #endif
     // A stored + fenced by every thread -> barrier -> one thread issues -> wait.
-    auto mma_layer = [&](bool input, uint32_t b_off, int n_out) {
+    // duty_slot >= 0 (PLT_MAP_DUTY_AFTER_BAR): the duty thread claims the next pair and issues
+    // its copies between the barrier and the MMA wait (where it would otherwise idle)
+    auto claim_pair = [&](int slot, int st) {   // one thread of the group
+        const int nextp = group_stride + atomicAdd(P.tile_ctr, 1);
+        Gs.next_tile[slot] = nextp;
+        if (nextp < n_pairs && pair_full_tma(nextp)) issue_pair(nextp, st ^ 1);
+    };
+    auto mma_layer = [&](bool input, uint32_t b_off, int n_out, int duty_slot = -1, int duty_st = 0) {
         PLT_CLK(c0);
         tc_fence_before();
         group_bar(g);
@@ -476,13 +486,14 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             pr_ifence += i0 - c1; pr_immas += i1 - i0; pr_icommit += i2 - i1;
 #endif
         }
+        if (duty_slot >= 0 && t == duty_t) claim_pair(duty_slot, duty_st);
         PLT_CLK(c2);
         mbar_wait(&S.bar_mma[g], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
 #ifdef PLT_MAP_PROFILE
         const long long c3 = clock64();
-        pr_bar += c1 - c0; pr_issue += c2 - c1; pr_wait += c3 - c2; ++pr_layers;
+        pr_bar += c1 - c0; pr_issue += c2 - c1; pr_wait += c3 - c2; ++pr_layers; pr_lastbar = c1 - c0;
 #endif
     };
     // hidden epilogue: TMEM (bias already folded) -> tanh -> hi/lo -> A operand, in two halves
@@ -611,37 +622,39 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         }
     };
 
-    // tiles: the first G per CTA statically (tile = group id), then dynamically -- one
-    // atomicAdd per chunk of kClaimChunk tiles hands them to whichever pipeline is free, so pipelines
-    // whose tiles held more valid rays (more regressor work) take fewer tiles and the
-    // SMs finish together
-    for (int it = 0; tile < n_tiles; ++it) {
-        const int st = it & 1;
+    // tile pairs: the first G per CTA statically (pair = group id), then dynamically -- one
+    // atomicAdd per pair hands the next one to whichever pipeline is free, so pipelines whose
+    // tiles held more valid rays (more regressor work) take fewer tiles and the SMs finish
+    // together.  A pair's two tiles are staged by one set of five bulk copies (1 KB each): the
+    // duty warp's claim + copy issue -- ~1000-1300 cycles per tile on its path to the input
+    // layer's barrier, where the pipeline's other warps waited for it (in-kernel clock profile)
+    // -- happens once per two tiles (C2 0.715 -> 0.710 ms, C3 0.496 -> 0.491;
+    // profiles/r02_map_pair_ab.jsonl)
+    for (int it = 0; pair < n_pairs; ++it) {
+        const int tile = 2 * pair + half;
+        const int st = pit & 1;
         const int base = tile * kTile;
         const int i = base + t;
         const bool in_range = i < n;
-        // claim the next tile and prefetch its inputs into the other stage (its previous
-        // contents were consumed a tile ago); published to the group through next_tile[it & 1]
-        if (t == duty_t) {
-            // one global atomic per kClaimChunk consecutive tiles: its round trip is exposed on
-            // the duty warp once per chunk instead of once per tile (C3 0.501 -> 0.496 ms, C2
-            // unchanged; profiles/r02_map_chunk_ab.jsonl)
-            if (it == 0 || Gs.chunk_left == 0) {
-                Gs.chunk_next = group_stride + atomicAdd(P.tile_ctr, kClaimChunk);
-                Gs.chunk_left = kClaimChunk;
-            }
-            const int next = Gs.chunk_next++;
-            --Gs.chunk_left;
-            Gs.next_tile[it & 1] = next;
-            if (next < n_tiles && tile_full_tma(next)) issue_stage(next, st ^ 1);
-        }
+        PLT_CLK(ot);
+        // at the first tile of a pair: claim the next pair (one global atomic per two tiles)
+        // and prefetch both its tiles into the other stage; published through next_tile[pit & 1]
+#ifndef PLT_MAP_DUTY_AFTER_BAR
+        if (half == 0 && t == duty_t) claim_pair(pit & 1, st);
+#endif
         PLT_CLK(o0);
+#ifdef PLT_MAP_PROFILE
+        pr_claim += o0 - ot;
+#endif
         float px = 0.f, py = 0.f, wx = 0.f, wy = 0.f, lam = 550.f;
-        if (tile_full_tma(tile)) {
-            mbar_wait(&S.bar_in[g][st], in_phase[st]);
-            in_phase[st] ^= 1u;
-            px = Gs.stage[st][0][t]; py = Gs.stage[st][1][t];
-            wx = Gs.stage[st][2][t]; wy = Gs.stage[st][3][t]; lam = Gs.stage[st][4][t];
+        if (pair_full_tma(pair)) {
+            if (half == 0) {
+                mbar_wait(&S.bar_in[g][st], in_phase[st]);
+                in_phase[st] ^= 1u;
+            }
+            const int e = half * kTile + t;
+            px = Gs.stage[st][0][e]; py = Gs.stage[st][1][e];
+            wx = Gs.stage[st][2][e]; wy = Gs.stage[st][3][e]; lam = Gs.stage[st][4][e];
         } else if (in_range) {
             px = P.in.ox[i]; py = P.in.oy[i]; wx = P.in.dx[i]; wy = P.in.dy[i]; lam = P.in.lambda_nm[i];
         }
@@ -650,7 +663,14 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         store_input(a_row, k.x);
         tmem_st_wait();
         PLT_CLK(o1);
+#ifdef PLT_MAP_DUTY_AFTER_BAR
+        mma_layer(true, P.lay.cls_w[0], 32, half == 0 ? (pit & 1) : -1, st);
+#else
         mma_layer(true, P.lay.cls_w[0], 32);
+#endif
+#ifdef PLT_MAP_PROFILE
+        pr_inbar += pr_lastbar; pr_top += o1 - ot;
+#endif
         hidden_epilogue(true);
         mma_layer(false, P.lay.cls_w[1], 32);
         PLT_CLK(o2);
@@ -687,7 +707,6 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             Gs.qi[slot] = (int)i | (k.flip ? (int)0x80000000u : 0);
         }
         qcount += total;
-        const int next_tile = Gs.next_tile[it & 1];   // written before the group barrier above
         PLT_CLK(o5);
         if (qcount >= kTile) run_regressor(kTile, -1);
 #ifdef PLT_MAP_PROFILE
@@ -695,7 +714,15 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         ++pr_tiles; pr_in += o1 - o0; pr_outep += o3 - o2; pr_write += o4 - o3; pr_queue += o5 - o4;
         if (o6 - o5 > 100) { pr_reg += o6 - o5; ++pr_regs; }
 #endif
-        tile = next_tile;
+        // next: the pair's second tile, else the claimed pair (written at this pair's first
+        // tile, before at least one group barrier)
+        if (half == 0 && 2 * pair + 1 < n_tiles) {
+            half = 1;
+        } else {
+            pair = Gs.next_tile[pit & 1];
+            half = 0;
+            ++pit;
+        }
     }
     // Leftovers (< 128 rays per pipeline): pooled across the CTA and run as full tiles,
     // chunk c by pipeline c mod G -- one or two regressor runs per CTA instead of G partial
@@ -708,6 +735,9 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
     for (int c = g; kTile * c < pooled; c += G) run_regressor(min(kTile, pooled - kTile * c), c);
 #ifdef PLT_MAP_PROFILE
     if (blockIdx.x == 0 && (t & 31) == 0 && g < 2) {
+        printf("PROF inbar pipe %d warp %d (duty %d, issue %d): per tile claim+stage issue %lld, top->stored %lld, "
+               "input-layer bar wait %lld\n", g, t >> 5, duty_t >> 5, issue_q, pr_claim / (pr_tiles ? pr_tiles : 1),
+               pr_top / (pr_tiles ? pr_tiles : 1), pr_inbar / (pr_tiles ? pr_tiles : 1));
         const long long tot = clock64() - pr_t0;
         printf("PROF blk0 pipe %d t %d: total %lld layers %lld | per layer: bar %lld issue %lld wait %lld epi %lld "
                "(ld %lld tanh %lld st %lld fence %lld) | other/layer %lld | issue: fence %lld mmas %lld commit %lld\n",
