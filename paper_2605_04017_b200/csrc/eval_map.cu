@@ -452,14 +452,12 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
 #define PLT_CLK(v)
 #endif
     // A stored + fenced by every thread -> barrier -> one thread issues -> wait.
-    // duty_slot >= 0 (PLT_MAP_DUTY_AFTER_BAR): the duty thread claims the next pair and issues
-    // its copies between the barrier and the MMA wait (where it would otherwise idle)
     auto claim_pair = [&](int slot, int st) {   // one thread of the group
         const int nextp = group_stride + atomicAdd(P.tile_ctr, 1);
         Gs.next_tile[slot] = nextp;
         if (nextp < n_pairs && pair_full_tma(nextp)) issue_pair(nextp, st ^ 1);
     };
-    auto mma_layer = [&](bool input, uint32_t b_off, int n_out, int duty_slot = -1, int duty_st = 0) {
+    auto mma_layer = [&](bool input, uint32_t b_off, int n_out) {
         PLT_CLK(c0);
         tc_fence_before();
         group_bar(g);
@@ -486,7 +484,6 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
             pr_ifence += i0 - c1; pr_immas += i1 - i0; pr_icommit += i2 - i1;
 #endif
         }
-        if (duty_slot >= 0 && t == duty_t) claim_pair(duty_slot, duty_st);
         PLT_CLK(c2);
         mbar_wait(&S.bar_mma[g], mma_phase);
         mma_phase ^= 1u;
@@ -639,9 +636,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         PLT_CLK(ot);
         // at the first tile of a pair: claim the next pair (one global atomic per two tiles)
         // and prefetch both its tiles into the other stage; published through next_tile[pit & 1]
-#ifndef PLT_MAP_DUTY_AFTER_BAR
         if (half == 0 && t == duty_t) claim_pair(pit & 1, st);
-#endif
         PLT_CLK(o0);
 #ifdef PLT_MAP_PROFILE
         pr_claim += o0 - ot;
@@ -663,11 +658,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         store_input(a_row, k.x);
         tmem_st_wait();
         PLT_CLK(o1);
-#ifdef PLT_MAP_DUTY_AFTER_BAR
-        mma_layer(true, P.lay.cls_w[0], 32, half == 0 ? (pit & 1) : -1, st);
-#else
         mma_layer(true, P.lay.cls_w[0], 32);
-#endif
 #ifdef PLT_MAP_PROFILE
         pr_inbar += pr_lastbar; pr_top += o1 - ot;
 #endif
