@@ -336,25 +336,25 @@ __device__ __forceinline__ void issue_hidden_warp(uint32_t tmem_d, uint32_t tmem
 }
 
 // Classifier: last hidden layer + fp32 output layer, h = tanh(D) from TMEM, logit = b +
-// sum_j w[j] h[j] (weights broadcast from shared memory) -- no MMA round for the single
-// output.  The dot product issues as packed FFMA2 accumulating even / odd j in the two halves.
-__device__ __forceinline__ void output_epilogue_cls(uint32_t tmem_row, const float* W, const float* b, float& y) {
-    float2 acc = make_float2(0.f, 0.f);
+// sum_j w[j] h[j], no MMA round for the single output.  The weights are kernel-parameter
+// constants (constant-bank FFMA operands): no shared-memory loads through the MIO queue,
+// which the tanh bursts keep full (8 LDS.128 per row before; C2 0.711 -> 0.709 ms, C3 0.492
+// -> 0.491, profiles/r02_map_pair_ab.jsonl).  Even / odd j accumulate apart.
+__device__ __forceinline__ void output_epilogue_cls(uint32_t tmem_row, const MapParams& mp, float& y) {
+    float a0 = 0.f, a1 = 0.f;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         float v[16];
         tmem_ld16(tmem_row + 16 * half, v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = tanh_approx(v[j]);
-        const float4* w4 = reinterpret_cast<const float4*>(W + 16 * half);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-            const float4 w = w4[q4];
-            acc = __ffma2_rn(make_float2(w.x, w.y), make_float2(v[4 * q4], v[4 * q4 + 1]), acc);
-            acc = __ffma2_rn(make_float2(w.z, w.w), make_float2(v[4 * q4 + 2], v[4 * q4 + 3]), acc);
+        for (int j = 0; j < 16; j += 2) {
+            a0 = fmaf(mp.cls_w3[16 * half + j], v[j], a0);
+            a1 = fmaf(mp.cls_w3[16 * half + j + 1], v[j + 1], a1);
         }
     }
-    y = b[0] + (acc.x + acc.y);
+    y = mp.cls_b3 + (a0 + a1);
 }
 template <int G>
 __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_constant__ Params P) {
@@ -534,7 +534,6 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         pr_fence += e1 - f0; pr_epi += e1 - e0;
 #endif
     };
-    const float* outw = reinterpret_cast<const float*>(S.w + P.lay.out_off);
 
     int qhead = 0, qcount = 0;
     // regressor over queue entries [qhead, qhead + rows), rows <= 128; chunk >= 0: rows
@@ -666,7 +665,7 @@ __global__ void __launch_bounds__(128 * G, 1) eval_map_kernel(const __grid_const
         mma_layer(false, P.lay.cls_w[1], 32);
         PLT_CLK(o2);
         float logit;
-        output_epilogue_cls(tmem_row, outw + kOutClsW, outw + kOutClsB, logit);
+        output_epilogue_cls(tmem_row, P.mp, logit);
         PLT_CLK(o3);
         const bool valid = in_range && logit >= 0.f;     // g(x) = 1 <=> logit >= 0 (A13)
         // ---- mask word + zeros for blocked rays -----------------------------------------

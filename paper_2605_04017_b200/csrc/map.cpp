@@ -185,8 +185,8 @@ plt_map* parse_map(const plt_lens* lens, const uint8_t* blob, size_t len) {
                 continue;
             }
             if (l + 1 == nl) {   // classifier output layer: fp32 block
-                for (uint32_t k = 0; k < fi; ++k) outw[kOutClsW + k] = bf16_to_f(W[k]);
-                outw[kOutClsB] = b[0];
+                for (uint32_t k = 0; k < fi; ++k) outw[kOutClsW + k] = m->params.cls_w3[k] = bf16_to_f(W[k]);
+                outw[kOutClsB] = m->params.cls_b3 = b[0];
                 continue;
             }
             const uint32_t woff = head == 0 ? L.cls_w[l] : L.reg_w[l];

@@ -79,7 +79,8 @@ struct MapDims {
 //   hidden layer: N=32, K=48 (W[32] | b_hi b_lo 0.. | 0..)   -> 3072 B
 // The classifier's output layer (32->1) is evaluated in fp32 from the last hidden
 // activations (no MMA round): its weights (bf16 values widened) and bias live in an fp32
-// block at `out_off`: W[32], b, pad to 4.  The regressor's (32->6) is an MMA operand.
+// block at `out_off`: W[32], b, pad to 4 (eval_map reads the copy in MapParams.cls_w3 /
+// cls_b3 as kernel-parameter constants).  The regressor's (32->6) is an MMA operand.
 struct MapLayout {
     uint32_t cls_w[2];     // classifier input + hidden operands
     uint32_t reg_w[5];     // regressor input + 4 hidden operands
@@ -92,6 +93,7 @@ constexpr int kOutClsW = 0, kOutClsB = 32, kOutFloats = 36;
 struct MapParams {
     float in_lo[4], in_scale[4];   // x_hat = clamp((x - lo) * scale - 1, -1, 1), scale = 2/(hi-lo)
     float out_mid[6], out_half[6];
+    float cls_w3[32], cls_b3;      // classifier output layer (also in the weight image's fp32 block)
 };
 
 // ---------------------------------------------------------------------------
